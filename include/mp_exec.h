@@ -1,0 +1,125 @@
+/*
+ * mp_exec.h — C-ABI of the B200 plan executor (libmpexec.so).
+ *
+ * The reference (meshplan, pure Python) has no native boundary: its executor is
+ * the discrete-event simulator `simulate` (reference pkg/src/meshplan/sim.py:91-188),
+ * which advances a clock by a modeled `duration` for every `compute` instruction
+ * (reshard.py:382, sim.py:148-151) and by `transfer_time`/`collective_time` for
+ * every `send`/`all_gather` (sim.py:74-88).  The functions below are the device
+ * work those instructions stand for.  Each entry point cites the reference site
+ * whose modeled cost it replaces with real sm_100a work.
+ *
+ * Conventions
+ *   - plain pointers / sizes only; no torch types;
+ *   - every call takes a `void* stream` (a cudaStream_t; NULL = legacy stream);
+ *   - return 0 on success, non-zero on error; `mp_last_error()` returns the
+ *     per-thread message of the last failure;
+ *   - tensors are row-major with explicit element strides; bf16 = uint16 bits.
+ *
+ * Binding from the reference side is via ctypes (the reference is Python);
+ * see INTEGRATION.md.
+ */
+#ifndef MP_EXEC_H
+#define MP_EXEC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- library ------------------------------------------------------------ */
+
+/* ABI version (bumped on signature changes). */
+int mp_abi_version(void);
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* mp_last_error(void);
+
+/* Number of device kernels this library has launched since load (all entry
+ * points; used by bench.py for the `gpu_launches` claim). */
+uint64_t mp_launch_count(void);
+
+/* ---- GEMM ------------------------------------------------------------------
+ * Replaces the modeled local matmul of a chosen ParallelAlgorithm
+ * (sharding.py:255-299; its time is compute_time, costs.py:83-86) and the
+ * batched variant (loops b,i,j,k, sharding.py:217-218).
+ *
+ *   C[b0,b1] = alpha * A[b0,b1] @ B[b0,b1] + beta * C[b0,b1]      (fp32 accumulate)
+ *
+ * Operand descriptors are int64[6]:
+ *   {rows, cols, row_stride, col_stride, batch_stride0, batch_stride1}
+ * in elements, describing the LOGICAL operand (A is M x K, B is K x N, C is M x N).
+ * For A and B exactly one of row_stride / col_stride must be 1 (K-major or
+ * MN-major storage; both are read by TMA with 128-byte swizzle straight into
+ * the tcgen05 operand layout, so transposed operands are never materialised).
+ * C must have col_stride == 1.  A, B: bf16.  C: bf16 (c_dtype 0) or fp32 (1).
+ * epilogue: 0 none, 1 GeLU(tanh) applied to alpha*acc (beta must be 0).
+ */
+int mp_gemm_bf16(const void* A, const int64_t* a_desc,
+                 const void* B, const int64_t* b_desc,
+                 void* C, const int64_t* c_desc, int c_dtype,
+                 int64_t nbatch0, int64_t nbatch1,
+                 float alpha, float beta, int epilogue,
+                 void* stream);
+
+/* ---- elementwise / row ops (trivial members, intra.py:93-160) ------------- */
+
+/* y = gelu_tanh(x); bf16, n elements, contiguous. */
+int mp_gelu_fwd(const void* x, void* y, int64_t n, void* stream);
+/* dx = gelu_tanh'(x) * dy; bf16. */
+int mp_gelu_bwd(const void* x, const void* dy, void* dx, int64_t n, void* stream);
+/* y = a + b (bf16, contiguous). */
+int mp_add(const void* a, const void* b, void* y, int64_t n, void* stream);
+/* y = scale * x (bf16 -> bf16), used for the loss seed dL/dy. */
+int mp_scale(const void* x, void* y, float scale, int64_t n, void* stream);
+/* Sum of squares of x (bf16) accumulated into out[0] (fp32, atomically). */
+int mp_sumsq(const void* x, float* out, int64_t n, void* stream);
+
+/* Row softmax over the last dim of a [rows, cols] bf16 matrix (row stride ld),
+ * y = softmax(scale * x).  Complete rows only (softmax dim not split). */
+int mp_softmax_fwd(const void* x, void* y, int64_t rows, int64_t cols, int64_t ld,
+                   float scale, void* stream);
+/* Split-row variant (softmax dim sharded over a mesh axis, SURVEY §7 hard
+ * part 3): pass 1 writes per-row (max, sumexp) partials of the local columns;
+ * after an all-reduce of the partials (max then rescaled sum), pass 2
+ * normalises.  stats: fp32 [rows, 2]. */
+int mp_softmax_stats(const void* x, float* stats, int64_t rows, int64_t cols,
+                     int64_t ld, float scale, void* stream);
+int mp_softmax_apply(const void* x, const float* stats, void* y, int64_t rows,
+                     int64_t cols, int64_t ld, float scale, void* stream);
+/* dx = scale * y * (dy - rowsum(dy*y)); rowdot: optional fp32 [rows] holding
+ * the (already all-reduced) rowsum, or NULL to compute it locally. */
+int mp_softmax_bwd(const void* y, const void* dy, void* dx, const float* rowdot,
+                   int64_t rows, int64_t cols, int64_t ld, float scale, void* stream);
+/* rowdot[r] = sum_c dy[r,c]*y[r,c]  (fp32 out), for the split-row backward. */
+int mp_softmax_rowdot(const void* y, const void* dy, float* rowdot, int64_t rows,
+                      int64_t cols, int64_t ld, void* stream);
+
+/* ---- box pack / unpack (cross-mesh Transfer, reshard.py:32-37,97-108) -----
+ * Copies the sub-box [lo, lo+ext) of a strided tensor of rank <= 4 to / from
+ * a dense buffer.  dims/strides in elements, elem_bytes in {2,4}. */
+int mp_pack_box(const void* src, const int64_t* src_strides, const int64_t* lo,
+                const int64_t* ext, int rank, int elem_bytes, void* dst, void* stream);
+int mp_unpack_box(const void* src, void* dst, const int64_t* dst_strides,
+                  const int64_t* lo, const int64_t* ext, int rank, int elem_bytes,
+                  void* stream);
+
+/* ---- optimizer (weight update after the ZeRO rewrite, intra.py:404-424) ---
+ * Fused Adam over flat fp32 master/m/v/grad buffers, writing the bf16
+ * working copy; grad is scaled by grad_scale before use. */
+int mp_adam_step(float* master, float* m, float* v, const float* grad,
+                 void* param_bf16, int64_t n, float lr, float beta1, float beta2,
+                 float eps, float weight_decay, float grad_scale, int64_t step,
+                 void* stream);
+
+/* fp32 -> bf16 and bf16 -> fp32 casts (n elements, contiguous). */
+int mp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
+int mp_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream);
+/* y(fp32) += x(bf16)  (gradient accumulation of a bf16 partial). */
+int mp_accum_bf16_f32(const void* x, float* y, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MP_EXEC_H */

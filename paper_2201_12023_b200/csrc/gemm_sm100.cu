@@ -1,0 +1,420 @@
+// Local-shard GEMM of a ParallelAlgorithm (reference sharding.py:255-299): the
+// per-device matmul / batched matmul on `local_dims` (sharding.py:90-92).
+//
+// sm_100a design: persistent warp-specialised kernel, one CTA per SM.
+//   warp 0      TMA producer (one elected lane), 128B-swizzled tiles -> smem ring
+//   warp 1      TMEM allocator + tcgen05.mma issuer (one lane), fp32 accum in TMEM
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile t overlap the
+// mainloop of tile t+1.  Operands may be K-major or MN-major (transposed views of
+// the IR's transpose reshapes are read in place), with up to two batch dims
+// (head split/merge reshapes are strided views, read with rank-4 TMA maps).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <mutex>
+#include "common.cuh"
+#include "../../include/mp_exec.h"
+
+namespace mp {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+
+struct GemmParams {
+  int M, N, K;
+  int nb0, nb1;
+  int tiles_m, tiles_n, num_tiles, k_blocks;
+  int a_mn, b_mn;
+  void* C;
+  int64_t ldc, c_bs0, c_bs1;
+  int c_f32;
+  float alpha, beta;
+  int epi;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN>
+__device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off, int m, int n,
+                                            const uint32_t (&r)[32]) {
+  // r: 32 consecutive fp32 accumulator columns [n, n+32) of row m
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+  if (p.epi == 1) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+  }
+  const bool full = (n + 32 <= p.N);
+  if (p.c_f32) {
+    float* c = reinterpret_cast<float*>(p.C) + row_off + (int64_t)m * p.ldc + n;
+    if (full) {
+      float4* c4 = reinterpret_cast<float4*>(c);
+      if (p.beta != 0.f) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float4 o = c4[i];
+          v[4 * i + 0] += p.beta * o.x;
+          v[4 * i + 1] += p.beta * o.y;
+          v[4 * i + 2] += p.beta * o.z;
+          v[4 * i + 3] += p.beta * o.w;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        c4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else {
+      for (int i = 0; i < 32 && n + i < p.N; ++i)
+        c[i] = v[i] + (p.beta != 0.f ? p.beta * c[i] : 0.f);
+    }
+  } else {
+    uint16_t* c = reinterpret_cast<uint16_t*>(p.C) + row_off + (int64_t)m * p.ldc + n;
+    if (full) {
+      uint4* c4 = reinterpret_cast<uint4*>(c);
+      if (p.beta != 0.f) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 o = c4[i];
+          uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            v[8 * i + 2 * j] += p.beta * bf2f((uint16_t)(w[j] & 0xffff));
+            v[8 * i + 2 * j + 1] += p.beta * bf2f((uint16_t)(w[j] >> 16));
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        c4[i] = make_uint4(pack_bf2(v[8 * i + 0], v[8 * i + 1]), pack_bf2(v[8 * i + 2], v[8 * i + 3]),
+                           pack_bf2(v[8 * i + 4], v[8 * i + 5]), pack_bf2(v[8 * i + 6], v[8 * i + 7]));
+      }
+    } else {
+      for (int i = 0; i < 32 && n + i < p.N; ++i) {
+        float o = (p.beta != 0.f) ? p.beta * bf2f(c[i]) : 0.f;
+        c[i] = f2bf(v[i] + o);
+      }
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int tiles_mn = p.tiles_m * p.tiles_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int b = t / tiles_mn;
+        const int rem = t - b * tiles_mn;
+        const int mb = rem / p.tiles_n;
+        const int nb = rem - mb * p.tiles_n;
+        const int b0 = b / p.nb1, b1 = b - (b / p.nb1) * p.nb1;
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+          uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
+          const int k0 = kb * BK;
+          if (p.a_mn) {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_4d(&tmA, &full[stage], a_dst + i * 8192, m0 + 64 * i, k0, b1, b0);
+          } else {
+            tma_load_4d(&tmA, &full[stage], a_dst, k0, m0, b1, b0);
+          }
+          if (p.b_mn) {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_4d(&tmB, &full[stage], b_dst + i * 8192, n0 + 64 * i, k0, b1, b0);
+          } else {
+            tma_load_4d(&tmB, &full[stage], b_dst, k0, n0, b1, b0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(BM, BN, p.a_mn, p.b_mn);
+      // K-major: 8-row groups 1024 B apart, K step of 16 elems = +32 B inside the
+      // 128 B swizzle atom.  MN-major: 64-elem MN chunks 8 KB apart (LBO), 8-k-row
+      // groups 1024 B apart (SBO), K step of 16 = +2048 B.
+      const uint32_t a_lbo = p.a_mn ? 8192u : 16u, b_lbo = p.b_mn ? 8192u : 16u;
+      const uint32_t a_kstep = p.a_mn ? 2048u : 32u, b_kstep = p.b_mn ? 2048u : 32u;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(a_base + kk * a_kstep, a_lbo, 1024u);
+            const uint64_t bd = umma_desc_sw128(b_base + kk * b_kstep, b_lbo, 1024u);
+            tc_mma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // epilogue warps: TMEM lane quarter is fixed by (warp % 4)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const int b = t / tiles_mn;
+      const int rem = t - b * tiles_mn;
+      const int mb = rem / p.tiles_n;
+      const int nb = rem - mb * p.tiles_n;
+      const int b0 = b / p.nb1, b1 = b - (b / p.nb1) * p.nb1;
+      const int64_t row_off = (int64_t)b0 * p.c_bs0 + (int64_t)b1 * p.c_bs1;
+      const int m = mb * BM + row;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+        tmem_ld_wait();
+        const int n = nb * BN + c * 32;
+        if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// rank-4 map: {contig extent, outer extent, nb1, nb0} with element strides.
+static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, int64_t s1,
+                    int64_t nb1, int64_t bs1, int64_t nb0, int64_t bs0, int box0, int box1) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 1;
+  }
+  const int64_t eb = 2;
+  if (nb1 <= 1) bs1 = s1 * d1;
+  if (nb0 <= 1) bs0 = bs1 * (nb1 < 1 ? 1 : nb1);
+  cuuint64_t dims[4] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)(nb1 < 1 ? 1 : nb1),
+                        (cuuint64_t)(nb0 < 1 ? 1 : nb0)};
+  cuuint64_t strides[3] = {(cuuint64_t)(s1 * eb), (cuuint64_t)(bs1 * eb), (cuuint64_t)(bs0 * eb)};
+  for (int i = 0; i < 3; ++i) {
+    if (strides[i] % 16 != 0 || strides[i] == 0) {
+      set_error("gemm operand stride not a multiple of 16 bytes (need 8-element aligned rows)");
+      return 2;
+    }
+  }
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) {
+    set_error("gemm operand base pointer not 16-byte aligned");
+    return 2;
+  }
+  cuuint32_t box[4] = {(cuuint32_t)box0, (cuuint32_t)box1, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed with code " + std::to_string((int)r));
+    return 1;
+  }
+  return 0;
+}
+
+template <int BN>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams p,
+                       cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) {
+      set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      return 1;
+    }
+    configured = true;
+  }
+  p.tiles_n = (p.N + BN - 1) / BN;
+  p.num_tiles = p.tiles_m * p.tiles_n * p.nb0 * p.nb1;
+  int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
+  gemm_bf16_kernel<BN><<<grid, kThreads, Cfg::SMEM, stream>>>(ma, mb, p);
+  return 0;
+}
+
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" int mp_gemm_bf16(const void* A, const int64_t* ad, const void* B, const int64_t* bd,
+                            void* C, const int64_t* cd, int c_dtype, int64_t nbatch0,
+                            int64_t nbatch1, float alpha, float beta, int epilogue,
+                            void* stream) {
+  clear_error();
+  MP_CHECK_ARG(A && B && C && ad && bd && cd, "null argument");
+  const int64_t M = ad[0], K = ad[1], N = bd[1];
+  MP_CHECK_ARG(bd[0] == K, "A cols != B rows");
+  MP_CHECK_ARG(cd[0] == M && cd[1] == N, "C shape mismatch");
+  MP_CHECK_ARG(M > 0 && N > 0 && K > 0, "empty gemm");
+  MP_CHECK_ARG(M < (1LL << 31) && N < (1LL << 31) && K < (1LL << 31), "gemm dims too large");
+  MP_CHECK_ARG(cd[3] == 1, "C must have unit column stride");
+  MP_CHECK_ARG(c_dtype == 0 || c_dtype == 1, "c_dtype must be 0 (bf16) or 1 (f32)");
+  MP_CHECK_ARG(epilogue == 0 || (epilogue == 1 && beta == 0.f), "bad epilogue");
+  MP_CHECK_ARG(nbatch0 >= 1 && nbatch1 >= 1, "bad batch extents");
+  MP_CHECK_ARG(reinterpret_cast<uintptr_t>(C) % 16 == 0 && cd[2] % (c_dtype ? 4 : 8) == 0,
+               "C must be 16-byte aligned with 16-byte aligned rows");
+
+  GemmParams p{};
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.nb0 = (int)nbatch0;
+  p.nb1 = (int)nbatch1;
+  p.tiles_m = (int)((M + BM - 1) / BM);
+  p.k_blocks = (int)((K + BK - 1) / BK);
+  p.C = C;
+  p.ldc = cd[2];
+  p.c_bs0 = cd[4];
+  p.c_bs1 = cd[5];
+  p.c_f32 = c_dtype;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.epi = epilogue;
+
+  // A (M x K): K-major if col stride 1, else MN-major (row stride 1).
+  CUtensorMap ma, mb;
+  int rc;
+  if (ad[3] == 1) {
+    p.a_mn = 0;
+    rc = make_map(&ma, A, K, M, ad[2], nbatch1, ad[5], nbatch0, ad[4], BK, BM);
+  } else if (ad[2] == 1) {
+    p.a_mn = 1;
+    rc = make_map(&ma, A, M, K, ad[3], nbatch1, ad[5], nbatch0, ad[4], 64, BK);
+  } else {
+    set_error("mp_gemm_bf16: A needs a unit stride");
+    return 2;
+  }
+  if (rc) return rc;
+
+  // B (K x N): MN-major if col stride 1, K-major if row stride 1.
+  int BN = (N > 128) ? 256 : (N > 64 ? 128 : 64);
+  if (bd[3] == 1) {
+    p.b_mn = 1;
+    rc = make_map(&mb, B, N, K, bd[2], nbatch1, bd[5], nbatch0, bd[4], 64, BK);
+  } else if (bd[2] == 1) {
+    p.b_mn = 0;
+    rc = make_map(&mb, B, K, N, bd[3], nbatch1, bd[5], nbatch0, bd[4], BK, BN);
+  } else {
+    set_error("mp_gemm_bf16: B needs a unit stride");
+    return 2;
+  }
+  if (rc) return rc;
+
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (BN == 256)
+    rc = launch_gemm<256>(ma, mb, p, s);
+  else if (BN == 128)
+    rc = launch_gemm<128>(ma, mb, p, s);
+  else
+    rc = launch_gemm<64>(ma, mb, p, s);
+  if (rc) return rc;
+  MP_CHECK_LAUNCH();
+  return 0;
+}

@@ -1,0 +1,606 @@
+// Memory-bound kernels of the plan executor: trivial-member ops (elementwise /
+// softmax, reference intra.py:93-160 merge + propagate), box pack/unpack for
+// cross-mesh transfers (reshard.py:97-157), the fused optimizer step and casts.
+// All are HBM-bound: 16-byte vector accesses, grid sized in multiples of the SM
+// count, one warp per row for row ops.
+#include <cuda_runtime.h>
+#include <atomic>
+#include <mutex>
+#include "common.cuh"
+#include "../../include/mp_exec.h"
+
+namespace mp {
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+void clear_error() { g_err.clear(); }
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int num_sms() {
+  static int dev_sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!dev_sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    dev_sms[dev] = v > 0 ? v : 148;
+  }
+  return dev_sms[dev];
+}
+
+static inline int grid_for(int64_t work_items, int threads) {
+  int64_t blocks = (work_items + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+// ------------------------------------------------------------ elementwise (bf16)
+// Vector path handles 8 elements per 16-byte access; tail is scalar.
+template <typename F>
+__global__ void unary_bf16_kernel(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
+                                  int64_t n, F f) {
+  const int64_t nv = n / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 a = reinterpret_cast<const uint4*>(x)[i];
+    uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      w[j] = pack_bf2(f(bf2f(w[j] & 0xffff)), f(bf2f(w[j] >> 16)));
+    reinterpret_cast<uint4*>(y)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  for (int64_t i = nv * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    y[i] = f2bf(f(bf2f(x[i])));
+}
+
+template <typename F>
+__global__ void binary_bf16_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ b,
+                                   uint16_t* __restrict__ y, int64_t n, F f) {
+  const int64_t nv = n / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 u = reinterpret_cast<const uint4*>(a)[i];
+    uint4 v = reinterpret_cast<const uint4*>(b)[i];
+    uint32_t wa[4] = {u.x, u.y, u.z, u.w}, wb[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      wa[j] = pack_bf2(f(bf2f(wa[j] & 0xffff), bf2f(wb[j] & 0xffff)),
+                       f(bf2f(wa[j] >> 16), bf2f(wb[j] >> 16)));
+    reinterpret_cast<uint4*>(y)[i] = make_uint4(wa[0], wa[1], wa[2], wa[3]);
+  }
+  for (int64_t i = nv * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    y[i] = f2bf(f(bf2f(a[i]), bf2f(b[i])));
+}
+
+struct GeluF {
+  __device__ float operator()(float x) const { return gelu_tanh(x); }
+};
+struct GeluBwdF {
+  __device__ float operator()(float x, float g) const { return gelu_tanh_grad(x) * g; }
+};
+struct AddF {
+  __device__ float operator()(float a, float b) const { return a + b; }
+};
+struct ScaleF {
+  float s;
+  __device__ float operator()(float x) const { return s * x; }
+};
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+__global__ void sumsq_kernel(const uint16_t* __restrict__ x, float* out, int64_t n) {
+  float acc = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nv = n / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 a = reinterpret_cast<const uint4*>(x)[i];
+    uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float lo = bf2f(w[j] & 0xffff), hi = bf2f(w[j] >> 16);
+      acc += lo * lo + hi * hi;
+    }
+  }
+  for (int64_t i = nv * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float v = bf2f(x[i]);
+    acc += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ float red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(out, v);
+  }
+}
+
+// ------------------------------------------------------------ softmax rows
+// One warp per row; row length arbitrary; two passes over the row (the second
+// hits L1/L2).  Inputs bf16, math fp32.
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// local (max, sumexp) of scale*x over the row; online merge per lane
+__device__ __forceinline__ void row_stats(const uint16_t* __restrict__ xr, int64_t cols,
+                                          float scale, int lane, float& m_out, float& s_out) {
+  float m = -INFINITY, s = 0.f;
+  const bool vec = ((cols & 7) == 0) && ((reinterpret_cast<uintptr_t>(xr) & 15) == 0);
+  if (vec) {
+    for (int64_t c = (int64_t)lane * 8; c < cols; c += 256) {
+      uint4 a = *reinterpret_cast<const uint4*>(xr + c);
+      uint32_t w[4] = {a.x, a.y, a.z, a.w};
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[2 * j] = scale * bf2f(w[j] & 0xffff);
+        v[2 * j + 1] = scale * bf2f(w[j] >> 16);
+      }
+      float lm = v[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) lm = fmaxf(lm, v[j]);
+      float nm = fmaxf(m, lm);
+      float acc = s * __expf(m - nm);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += __expf(v[j] - nm);
+      m = nm;
+      s = acc;
+    }
+  } else {
+    for (int64_t c = lane; c < cols; c += 32) {
+      float v = scale * bf2f(xr[c]);
+      float nm = fmaxf(m, v);
+      s = s * __expf(m - nm) + __expf(v - nm);
+      m = nm;
+    }
+  }
+  float gm = warp_max(m);
+  float ls = (m == -INFINITY) ? 0.f : s * __expf(m - gm);
+  m_out = gm;
+  s_out = warp_sum(ls);
+}
+
+__device__ __forceinline__ void row_write(const uint16_t* __restrict__ xr, uint16_t* __restrict__ yr,
+                                          int64_t cols, float scale, float m, float inv, int lane) {
+  const bool vec = ((cols & 7) == 0) && ((reinterpret_cast<uintptr_t>(xr) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(yr) & 15) == 0);
+  if (vec) {
+    for (int64_t c = (int64_t)lane * 8; c < cols; c += 256) {
+      uint4 a = *reinterpret_cast<const uint4*>(xr + c);
+      uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        w[j] = pack_bf2(__expf(scale * bf2f(w[j] & 0xffff) - m) * inv,
+                        __expf(scale * bf2f(w[j] >> 16) - m) * inv);
+      *reinterpret_cast<uint4*>(yr + c) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  } else {
+    for (int64_t c = lane; c < cols; c += 32) yr[c] = f2bf(__expf(scale * bf2f(xr[c]) - m) * inv);
+  }
+}
+
+__global__ void softmax_fwd_kernel(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
+                                   int64_t rows, int64_t cols, int64_t ld, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb) {
+    const uint16_t* xr = x + r * ld;
+    float m, s;
+    row_stats(xr, cols, scale, lane, m, s);
+    row_write(xr, y + r * ld, cols, scale, m, 1.f / s, lane);
+  }
+}
+
+__global__ void softmax_stats_kernel(const uint16_t* __restrict__ x, float* __restrict__ stats,
+                                     int64_t rows, int64_t cols, int64_t ld, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb) {
+    float m, s;
+    row_stats(x + r * ld, cols, scale, lane, m, s);
+    if (lane == 0) {
+      stats[2 * r] = m;
+      stats[2 * r + 1] = s;
+    }
+  }
+}
+
+__global__ void softmax_apply_kernel(const uint16_t* __restrict__ x, const float* __restrict__ stats,
+                                     uint16_t* __restrict__ y, int64_t rows, int64_t cols,
+                                     int64_t ld, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb)
+    row_write(x + r * ld, y + r * ld, cols, scale, stats[2 * r], 1.f / stats[2 * r + 1], lane);
+}
+
+__device__ __forceinline__ float row_dot(const uint16_t* __restrict__ yr,
+                                         const uint16_t* __restrict__ gr, int64_t cols, int lane) {
+  float acc = 0.f;
+  const bool vec = ((cols & 7) == 0) && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(gr) & 15) == 0);
+  if (vec) {
+    for (int64_t c = (int64_t)lane * 8; c < cols; c += 256) {
+      uint4 a = *reinterpret_cast<const uint4*>(yr + c);
+      uint4 b = *reinterpret_cast<const uint4*>(gr + c);
+      uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        acc += bf2f(wa[j] & 0xffff) * bf2f(wb[j] & 0xffff) + bf2f(wa[j] >> 16) * bf2f(wb[j] >> 16);
+    }
+  } else {
+    for (int64_t c = lane; c < cols; c += 32) acc += bf2f(yr[c]) * bf2f(gr[c]);
+  }
+  return warp_sum(acc);
+}
+
+__global__ void softmax_rowdot_kernel(const uint16_t* __restrict__ y, const uint16_t* __restrict__ g,
+                                      float* __restrict__ out, int64_t rows, int64_t cols,
+                                      int64_t ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb) {
+    float d = row_dot(y + r * ld, g + r * ld, cols, lane);
+    if (lane == 0) out[r] = d;
+  }
+}
+
+__global__ void softmax_bwd_kernel(const uint16_t* __restrict__ y, const uint16_t* __restrict__ g,
+                                   uint16_t* __restrict__ dx, const float* __restrict__ rowdot,
+                                   int64_t rows, int64_t cols, int64_t ld, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb) {
+    const uint16_t* yr = y + r * ld;
+    const uint16_t* gr = g + r * ld;
+    uint16_t* dr = dx + r * ld;
+    float d = rowdot ? rowdot[r] : row_dot(yr, gr, cols, lane);
+    const bool vec = ((cols & 7) == 0) && ((reinterpret_cast<uintptr_t>(yr) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(gr) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(dr) & 15) == 0);
+    if (vec) {
+      for (int64_t c = (int64_t)lane * 8; c < cols; c += 256) {
+        uint4 a = *reinterpret_cast<const uint4*>(yr + c);
+        uint4 b = *reinterpret_cast<const uint4*>(gr + c);
+        uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float y0 = bf2f(wa[j] & 0xffff), y1 = bf2f(wa[j] >> 16);
+          float g0 = bf2f(wb[j] & 0xffff), g1 = bf2f(wb[j] >> 16);
+          wa[j] = pack_bf2(scale * y0 * (g0 - d), scale * y1 * (g1 - d));
+        }
+        *reinterpret_cast<uint4*>(dr + c) = make_uint4(wa[0], wa[1], wa[2], wa[3]);
+      }
+    } else {
+      for (int64_t c = lane; c < cols; c += 32) {
+        float yy = bf2f(yr[c]);
+        dr[c] = f2bf(scale * yy * (bf2f(gr[c]) - d));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ box pack / unpack
+struct BoxArgs {
+  int64_t ext[4];
+  int64_t str[4];  // strides of the strided side, elements
+  int64_t off;     // element offset of lo on the strided side
+  int rank;
+};
+
+template <typename T, bool PACK>
+__global__ void box_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, BoxArgs a,
+                                int64_t total) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+    int64_t rem = i, off = a.off;
+#pragma unroll
+    for (int d = 3; d >= 0; --d) {
+      if (d < a.rank) {
+        int64_t c = rem % a.ext[d];
+        rem /= a.ext[d];
+        off += c * a.str[d];
+      }
+    }
+    if (PACK)
+      dst[i] = src[off];
+    else
+      dst[off] = src[i];
+  }
+}
+
+static int box_copy(const void* src, void* dst, const int64_t* strides, const int64_t* lo,
+                    const int64_t* ext, int rank, int elem_bytes, bool pack, cudaStream_t s) {
+  if (rank < 1 || rank > 4) {
+    set_error("box rank must be 1..4");
+    return 2;
+  }
+  BoxArgs a{};
+  a.rank = rank;
+  a.off = 0;
+  int64_t total = 1;
+  for (int d = 0; d < rank; ++d) {
+    a.ext[d] = ext[d];
+    a.str[d] = strides[d];
+    a.off += lo[d] * strides[d];
+    total *= ext[d];
+  }
+  if (total == 0) return 0;
+  // Vectorise the innermost dim when it is unit-stride and 16-byte divisible.
+  int vec = 1;
+  if (strides[rank - 1] == 1) {
+    const int64_t inner_b = ext[rank - 1] * elem_bytes;
+    bool ok = (inner_b % 16 == 0) && ((a.off * elem_bytes) % 16 == 0) && aligned16(src) &&
+              aligned16(dst);
+    for (int d = 0; d < rank - 1 && ok; ++d) ok = ((strides[d] * elem_bytes) % 16 == 0);
+    if (ok) vec = 16 / elem_bytes;
+  }
+  const int threads = 256;
+  if (vec > 1) {
+    BoxArgs v = a;
+    v.ext[rank - 1] = a.ext[rank - 1] / vec;
+    for (int d = 0; d < rank - 1; ++d) v.str[d] = a.str[d] / vec;
+    v.str[rank - 1] = 1;
+    v.off = a.off / vec;
+    int64_t tv = total / vec;
+    if (pack)
+      box_copy_kernel<uint4, true><<<grid_for(tv, threads), threads, 0, s>>>(
+          (const uint4*)src, (uint4*)dst, v, tv);
+    else
+      box_copy_kernel<uint4, false><<<grid_for(tv, threads), threads, 0, s>>>(
+          (const uint4*)src, (uint4*)dst, v, tv);
+  } else if (elem_bytes == 2) {
+    if (pack)
+      box_copy_kernel<uint16_t, true><<<grid_for(total, threads), threads, 0, s>>>(
+          (const uint16_t*)src, (uint16_t*)dst, a, total);
+    else
+      box_copy_kernel<uint16_t, false><<<grid_for(total, threads), threads, 0, s>>>(
+          (const uint16_t*)src, (uint16_t*)dst, a, total);
+  } else if (elem_bytes == 4) {
+    if (pack)
+      box_copy_kernel<uint32_t, true><<<grid_for(total, threads), threads, 0, s>>>(
+          (const uint32_t*)src, (uint32_t*)dst, a, total);
+    else
+      box_copy_kernel<uint32_t, false><<<grid_for(total, threads), threads, 0, s>>>(
+          (const uint32_t*)src, (uint32_t*)dst, a, total);
+  } else {
+    set_error("elem_bytes must be 2 or 4");
+    return 2;
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------ optimizer / casts
+__global__ void adam_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
+                            const float* __restrict__ g, uint16_t* __restrict__ p, int64_t n,
+                            float lr, float b1, float b2, float eps, float wd, float gscale,
+                            float bc1, float bc2) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float gi = g[i] * gscale;
+    float mi = b1 * m[i] + (1.f - b1) * gi;
+    float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    float w = master[i];
+    float upd = (mi / bc1) / (sqrtf(vi / bc2) + eps) + wd * w;
+    w -= lr * upd;
+    master[i] = w;
+    p[i] = f2bf(w);
+  }
+}
+
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ x, uint16_t* __restrict__ y, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) y[i] = f2bf(x[i]);
+}
+__global__ void cast_bf16_f32_kernel(const uint16_t* __restrict__ x, float* __restrict__ y, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) y[i] = bf2f(x[i]);
+}
+__global__ void accum_bf16_f32_kernel(const uint16_t* __restrict__ x, float* __restrict__ y, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) y[i] += bf2f(x[i]);
+}
+
+}  // namespace mp
+
+using namespace mp;
+
+#define MP_STREAM(s) reinterpret_cast<cudaStream_t>(s)
+
+extern "C" {
+
+int mp_abi_version(void) { return 1; }
+const char* mp_last_error(void) { return g_err.c_str(); }
+uint64_t mp_launch_count(void) { return g_launches.load(); }
+
+int mp_gelu_fwd(const void* x, void* y, int64_t n, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && y && n >= 0, "bad args");
+  MP_CHECK_ARG(aligned16(x) && aligned16(y), "pointers must be 16-byte aligned");
+  if (n == 0) return 0;
+  unary_bf16_kernel<<<grid_for((n + 7) / 8, 256), 256, 0, MP_STREAM(stream)>>>(
+      (const uint16_t*)x, (uint16_t*)y, n, GeluF{});
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_gelu_bwd(const void* x, const void* dy, void* dx, int64_t n, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && dy && dx && n >= 0, "bad args");
+  MP_CHECK_ARG(aligned16(x) && aligned16(dy) && aligned16(dx), "pointers must be 16-byte aligned");
+  if (n == 0) return 0;
+  binary_bf16_kernel<<<grid_for((n + 7) / 8, 256), 256, 0, MP_STREAM(stream)>>>(
+      (const uint16_t*)x, (const uint16_t*)dy, (uint16_t*)dx, n, GeluBwdF{});
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_add(const void* a, const void* b, void* y, int64_t n, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(a && b && y && n >= 0, "bad args");
+  MP_CHECK_ARG(aligned16(a) && aligned16(b) && aligned16(y), "pointers must be 16-byte aligned");
+  if (n == 0) return 0;
+  binary_bf16_kernel<<<grid_for((n + 7) / 8, 256), 256, 0, MP_STREAM(stream)>>>(
+      (const uint16_t*)a, (const uint16_t*)b, (uint16_t*)y, n, AddF{});
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_scale(const void* x, void* y, float scale, int64_t n, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && y && n >= 0, "bad args");
+  MP_CHECK_ARG(aligned16(x) && aligned16(y), "pointers must be 16-byte aligned");
+  if (n == 0) return 0;
+  unary_bf16_kernel<<<grid_for((n + 7) / 8, 256), 256, 0, MP_STREAM(stream)>>>(
+      (const uint16_t*)x, (uint16_t*)y, n, ScaleF{scale});
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_sumsq(const void* x, float* out, int64_t n, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && out && n >= 0, "bad args");
+  MP_CHECK_ARG(aligned16(x), "pointer must be 16-byte aligned");
+  if (n == 0) return 0;
+  sumsq_kernel<<<grid_for((n + 7) / 8, 256), 256, 0, MP_STREAM(stream)>>>((const uint16_t*)x, out, n);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+static int row_grid(int64_t rows) { return grid_for(rows * 32, 256); }
+
+int mp_softmax_fwd(const void* x, void* y, int64_t rows, int64_t cols, int64_t ld, float scale,
+                   void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && y && rows >= 0 && cols > 0 && ld >= cols, "bad args");
+  if (rows == 0) return 0;
+  softmax_fwd_kernel<<<row_grid(rows), 256, 0, MP_STREAM(stream)>>>(
+      (const uint16_t*)x, (uint16_t*)y, rows, cols, ld, scale);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_softmax_stats(const void* x, float* stats, int64_t rows, int64_t cols, int64_t ld,
+                     float scale, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && stats && rows >= 0 && cols > 0 && ld >= cols, "bad args");
+  if (rows == 0) return 0;
+  softmax_stats_kernel<<<row_grid(rows), 256, 0, MP_STREAM(stream)>>>((const uint16_t*)x, stats,
+                                                                      rows, cols, ld, scale);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_softmax_apply(const void* x, const float* stats, void* y, int64_t rows, int64_t cols,
+                     int64_t ld, float scale, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && stats && y && rows >= 0 && cols > 0 && ld >= cols, "bad args");
+  if (rows == 0) return 0;
+  softmax_apply_kernel<<<row_grid(rows), 256, 0, MP_STREAM(stream)>>>(
+      (const uint16_t*)x, stats, (uint16_t*)y, rows, cols, ld, scale);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_softmax_bwd(const void* y, const void* dy, void* dx, const float* rowdot, int64_t rows,
+                   int64_t cols, int64_t ld, float scale, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(y && dy && dx && rows >= 0 && cols > 0 && ld >= cols, "bad args");
+  if (rows == 0) return 0;
+  softmax_bwd_kernel<<<row_grid(rows), 256, 0, MP_STREAM(stream)>>>(
+      (const uint16_t*)y, (const uint16_t*)dy, (uint16_t*)dx, rowdot, rows, cols, ld, scale);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_softmax_rowdot(const void* y, const void* dy, float* rowdot, int64_t rows, int64_t cols,
+                      int64_t ld, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(y && dy && rowdot && rows >= 0 && cols > 0 && ld >= cols, "bad args");
+  if (rows == 0) return 0;
+  softmax_rowdot_kernel<<<row_grid(rows), 256, 0, MP_STREAM(stream)>>>(
+      (const uint16_t*)y, (const uint16_t*)dy, rowdot, rows, cols, ld);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_pack_box(const void* src, const int64_t* src_strides, const int64_t* lo, const int64_t* ext,
+                int rank, int elem_bytes, void* dst, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(src && dst && src_strides && lo && ext, "null argument");
+  int rc = box_copy(src, dst, src_strides, lo, ext, rank, elem_bytes, true, MP_STREAM(stream));
+  if (rc) return rc;
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_unpack_box(const void* src, void* dst, const int64_t* dst_strides, const int64_t* lo,
+                  const int64_t* ext, int rank, int elem_bytes, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(src && dst && dst_strides && lo && ext, "null argument");
+  int rc = box_copy(src, dst, dst_strides, lo, ext, rank, elem_bytes, false, MP_STREAM(stream));
+  if (rc) return rc;
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_adam_step(float* master, float* m, float* v, const float* grad, void* param_bf16, int64_t n,
+                 float lr, float beta1, float beta2, float eps, float weight_decay,
+                 float grad_scale, int64_t step, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(master && m && v && grad && param_bf16 && n >= 0 && step >= 1, "bad args");
+  if (n == 0) return 0;
+  float bc1 = 1.f - powf(beta1, (float)step);
+  float bc2 = 1.f - powf(beta2, (float)step);
+  adam_kernel<<<grid_for(n, 256), 256, 0, MP_STREAM(stream)>>>(
+      master, m, v, grad, (uint16_t*)param_bf16, n, lr, beta1, beta2, eps, weight_decay,
+      grad_scale, bc1, bc2);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && y && n >= 0, "bad args");
+  if (n == 0) return 0;
+  cast_f32_bf16_kernel<<<grid_for(n, 256), 256, 0, MP_STREAM(stream)>>>(x, (uint16_t*)y, n);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && y && n >= 0, "bad args");
+  if (n == 0) return 0;
+  cast_bf16_f32_kernel<<<grid_for(n, 256), 256, 0, MP_STREAM(stream)>>>((const uint16_t*)x, y, n);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_accum_bf16_f32(const void* x, float* y, int64_t n, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(x && y && n >= 0, "bad args");
+  if (n == 0) return 0;
+  accum_bf16_f32_kernel<<<grid_for(n, 256), 256, 0, MP_STREAM(stream)>>>((const uint16_t*)x, y, n);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,325 @@
+"""ctypes binding of libmpexec.so (include/mp_exec.h) plus torch-tensor helpers.
+
+This is the only door from the host runtime to device work.  There is no
+fallback: if the library is missing or a call fails, a NativeError is raised
+(the reference's errors are exceptions too, e.g. SimError at sim.py:26).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from pathlib import Path
+from typing import Optional
+
+import torch
+
+_LIB_PATH = Path(__file__).resolve().parent / "libmpexec.so"
+_lib: Optional[ctypes.CDLL] = None
+
+c_i64 = ctypes.c_int64
+c_int = ctypes.c_int
+c_f32 = ctypes.c_float
+c_vp = ctypes.c_void_p
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+
+EXPORTS = {
+    "mp_abi_version": ([], c_int),
+    "mp_last_error": ([], ctypes.c_char_p),
+    "mp_launch_count": ([], ctypes.c_uint64),
+    "mp_gemm_bf16": ([c_vp, c_i64p, c_vp, c_i64p, c_vp, c_i64p, c_int, c_i64, c_i64,
+                      c_f32, c_f32, c_int, c_vp], c_int),
+    "mp_gelu_fwd": ([c_vp, c_vp, c_i64, c_vp], c_int),
+    "mp_gelu_bwd": ([c_vp, c_vp, c_vp, c_i64, c_vp], c_int),
+    "mp_add": ([c_vp, c_vp, c_vp, c_i64, c_vp], c_int),
+    "mp_scale": ([c_vp, c_vp, c_f32, c_i64, c_vp], c_int),
+    "mp_sumsq": ([c_vp, c_vp, c_i64, c_vp], c_int),
+    "mp_softmax_fwd": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
+    "mp_softmax_stats": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
+    "mp_softmax_apply": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
+    "mp_softmax_bwd": ([c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
+    "mp_softmax_rowdot": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp], c_int),
+    "mp_pack_box": ([c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp, c_vp], c_int),
+    "mp_unpack_box": ([c_vp, c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp], c_int),
+    "mp_adam_step": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_f32, c_f32, c_f32, c_f32, c_f32,
+                      c_f32, c_i64, c_vp], c_int),
+    "mp_cast_f32_bf16": ([c_vp, c_vp, c_i64, c_vp], c_int),
+    "mp_cast_bf16_f32": ([c_vp, c_vp, c_i64, c_vp], c_int),
+    "mp_accum_bf16_f32": ([c_vp, c_vp, c_i64, c_vp], c_int),
+}
+
+
+class NativeError(RuntimeError):
+    """A libmpexec call failed (or the library is absent)."""
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load(path: Optional[Path] = None) -> ctypes.CDLL:
+    """Load libmpexec.so and bind every exported symbol; raises if anything is
+    missing.  Never falls back to another implementation."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path or os.environ.get("MPEXEC_LIB", _LIB_PATH))
+    if not p.exists():
+        raise NativeError(f"{p} not built; run `python -m paper_2201_12023_b200.build_native`")
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in EXPORTS.items():
+        fn = getattr(lib, name, None)
+        if fn is None:
+            raise NativeError(f"{p} does not export {name}")
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().mp_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed (rc={rc}): {msg}")
+
+
+def launch_count() -> int:
+    return int(load().mp_launch_count())
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _arr(vals) -> ctypes.Array:
+    return (ctypes.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+def _require(t: torch.Tensor, dtype: torch.dtype, name: str) -> None:
+    if not t.is_cuda:
+        raise NativeError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != dtype:
+        raise NativeError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+# --------------------------------------------------------------------------- GEMM
+
+def _split_batch(t: torch.Tensor, name: str):
+    """(…, R, C) view -> (descriptor[6], batch extents (nb0, nb1)).  Up to two
+    batch dims; a 1-batch-dim view uses (1, n)."""
+    if t.dim() < 2 or t.dim() > 4:
+        raise NativeError(f"{name}: rank {t.dim()} unsupported (2..4)")
+    r, c = t.shape[-2], t.shape[-1]
+    rs, cs = t.stride(-2), t.stride(-1)
+    if r == 1:
+        rs = cs * c if cs == 1 else 1
+    if c == 1:
+        cs = 1 if rs != 1 else r
+    if t.dim() == 2:
+        return [r, c, rs, cs, 0, 0], (1, 1)
+    if t.dim() == 3:
+        return [r, c, rs, cs, 0, t.stride(0)], (1, t.shape[0])
+    return [r, c, rs, cs, t.stride(0), t.stride(1)], (t.shape[0], t.shape[1])
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 1.0,
+         beta: float = 0.0, gelu: bool = False, stream=None) -> torch.Tensor:
+    """out = alpha * a @ b + beta * out on the tcgen05 kernel.  a: (…, M, K),
+    b: (…, K, N) bf16 views (any of K-/MN-major), out: (…, M, N) bf16 or fp32
+    with unit column stride.  Batch dims must agree."""
+    _require(a, torch.bfloat16, "a")
+    _require(b, torch.bfloat16, "b")
+    if out.dtype not in (torch.bfloat16, torch.float32):
+        raise NativeError("out must be bf16 or fp32")
+    ad, ab = _split_batch(a, "a")
+    bd, bb = _split_batch(b, "b")
+    cd, cb = _split_batch(out, "out")
+    if not (ab == bb == cb):
+        raise NativeError(f"batch mismatch {ab} {bb} {cb}")
+    rc = load().mp_gemm_bf16(a.data_ptr(), _arr(ad), b.data_ptr(), _arr(bd), out.data_ptr(),
+                             _arr(cd), 1 if out.dtype == torch.float32 else 0, ab[0], ab[1],
+                             float(alpha), float(beta), 1 if gelu else 0, _stream(stream))
+    _check(rc, "mp_gemm_bf16")
+    return out
+
+
+# --------------------------------------------------------------------------- elementwise
+
+def _contig(t: torch.Tensor, name: str) -> None:
+    if not t.is_contiguous():
+        raise NativeError(f"{name} must be contiguous")
+
+
+def gelu(x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    _require(x, torch.bfloat16, "x")
+    _contig(x, "x")
+    out = torch.empty_like(x) if out is None else out
+    _check(load().mp_gelu_fwd(x.data_ptr(), out.data_ptr(), x.numel(), _stream(stream)), "mp_gelu_fwd")
+    return out
+
+
+def gelu_bwd(x: torch.Tensor, dy: torch.Tensor, out: Optional[torch.Tensor] = None,
+             stream=None) -> torch.Tensor:
+    for t, n in ((x, "x"), (dy, "dy")):
+        _require(t, torch.bfloat16, n)
+        _contig(t, n)
+    out = torch.empty_like(x) if out is None else out
+    _check(load().mp_gelu_bwd(x.data_ptr(), dy.data_ptr(), out.data_ptr(), x.numel(),
+                              _stream(stream)), "mp_gelu_bwd")
+    return out
+
+
+def add(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None,
+        stream=None) -> torch.Tensor:
+    for t, n in ((a, "a"), (b, "b")):
+        _require(t, torch.bfloat16, n)
+        _contig(t, n)
+    if a.shape != b.shape:
+        raise NativeError(f"add shape mismatch {tuple(a.shape)} {tuple(b.shape)}")
+    out = torch.empty_like(a) if out is None else out
+    _check(load().mp_add(a.data_ptr(), b.data_ptr(), out.data_ptr(), a.numel(), _stream(stream)),
+           "mp_add")
+    return out
+
+
+def scale(x: torch.Tensor, s: float, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    _require(x, torch.bfloat16, "x")
+    _contig(x, "x")
+    out = torch.empty_like(x) if out is None else out
+    _check(load().mp_scale(x.data_ptr(), out.data_ptr(), float(s), x.numel(), _stream(stream)),
+           "mp_scale")
+    return out
+
+
+def sumsq(x: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    _require(x, torch.bfloat16, "x")
+    _contig(x, "x")
+    _require(out, torch.float32, "out")
+    _check(load().mp_sumsq(x.data_ptr(), out.data_ptr(), x.numel(), _stream(stream)), "mp_sumsq")
+    return out
+
+
+def _rows(x: torch.Tensor, name: str):
+    if x.stride(-1) != 1:
+        raise NativeError(f"{name}: last dim must be unit-stride")
+    cols = x.shape[-1]
+    rows = x.numel() // cols if cols else 0
+    # rows of a (…, cols) tensor must be equally spaced
+    ld = x.stride(-2) if x.dim() >= 2 else cols
+    if x.dim() > 2:
+        exp = ld * x.shape[-2]
+        for d in range(x.dim() - 3, -1, -1):
+            if x.stride(d) != exp:
+                raise NativeError(f"{name}: rows not uniformly strided")
+            exp *= x.shape[d]
+    return rows, cols, ld
+
+
+def softmax(x: torch.Tensor, s: float, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    _require(x, torch.bfloat16, "x")
+    out = torch.empty_like(x) if out is None else out
+    rows, cols, ld = _rows(x, "x")
+    if _rows(out, "out")[2] != ld:
+        raise NativeError("softmax out must share the input row stride")
+    _check(load().mp_softmax_fwd(x.data_ptr(), out.data_ptr(), rows, cols, ld, float(s),
+                                 _stream(stream)), "mp_softmax_fwd")
+    return out
+
+
+def softmax_stats(x: torch.Tensor, s: float, stats: torch.Tensor, stream=None) -> torch.Tensor:
+    _require(x, torch.bfloat16, "x")
+    _require(stats, torch.float32, "stats")
+    rows, cols, ld = _rows(x, "x")
+    _check(load().mp_softmax_stats(x.data_ptr(), stats.data_ptr(), rows, cols, ld, float(s),
+                                   _stream(stream)), "mp_softmax_stats")
+    return stats
+
+
+def softmax_apply(x: torch.Tensor, stats: torch.Tensor, s: float,
+                  out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    _require(x, torch.bfloat16, "x")
+    out = torch.empty_like(x) if out is None else out
+    rows, cols, ld = _rows(x, "x")
+    _check(load().mp_softmax_apply(x.data_ptr(), stats.data_ptr(), out.data_ptr(), rows, cols, ld,
+                                   float(s), _stream(stream)), "mp_softmax_apply")
+    return out
+
+
+def softmax_rowdot(y: torch.Tensor, dy: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    rows, cols, ld = _rows(y, "y")
+    _check(load().mp_softmax_rowdot(y.data_ptr(), dy.data_ptr(), out.data_ptr(), rows, cols, ld,
+                                    _stream(stream)), "mp_softmax_rowdot")
+    return out
+
+
+def softmax_bwd(y: torch.Tensor, dy: torch.Tensor, s: float, rowdot: Optional[torch.Tensor] = None,
+                out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    _require(y, torch.bfloat16, "y")
+    _require(dy, torch.bfloat16, "dy")
+    out = torch.empty_like(y) if out is None else out
+    rows, cols, ld = _rows(y, "y")
+    if _rows(dy, "dy")[2] != ld or _rows(out, "out")[2] != ld:
+        raise NativeError("softmax_bwd operands must share the row stride")
+    _check(load().mp_softmax_bwd(y.data_ptr(), dy.data_ptr(), out.data_ptr(),
+                                 rowdot.data_ptr() if rowdot is not None else None, rows, cols, ld,
+                                 float(s), _stream(stream)), "mp_softmax_bwd")
+    return out
+
+
+# --------------------------------------------------------------------------- boxes
+
+def pack_box(src: torch.Tensor, lo, ext, out: Optional[torch.Tensor] = None,
+             stream=None) -> torch.Tensor:
+    """Dense copy of src[lo:lo+ext] (src any strided view, rank <= 4)."""
+    if not src.is_cuda:
+        raise NativeError("pack_box: src must be CUDA")
+    rank = src.dim()
+    n = math.prod(ext)
+    out = torch.empty(n, dtype=src.dtype, device=src.device) if out is None else out
+    if n == 0:
+        return out
+    _check(load().mp_pack_box(src.data_ptr(), _arr(src.stride()), _arr(lo), _arr(ext), rank,
+                              src.element_size(), out.data_ptr(), _stream(stream)), "mp_pack_box")
+    return out
+
+
+def unpack_box(buf: torch.Tensor, dst: torch.Tensor, lo, ext, stream=None) -> None:
+    if not dst.is_cuda:
+        raise NativeError("unpack_box: dst must be CUDA")
+    if math.prod(ext) == 0:
+        return
+    _check(load().mp_unpack_box(buf.data_ptr(), dst.data_ptr(), _arr(dst.stride()), _arr(lo),
+                                _arr(ext), dst.dim(), dst.element_size(), _stream(stream)),
+           "mp_unpack_box")
+
+
+# --------------------------------------------------------------------------- optimizer / casts
+
+def adam_step(master, m, v, grad, param_bf16, *, lr, beta1, beta2, eps, weight_decay,
+              grad_scale, step, stream=None) -> None:
+    for t, n in ((master, "master"), (m, "m"), (v, "v"), (grad, "grad")):
+        _require(t, torch.float32, n)
+    _require(param_bf16, torch.bfloat16, "param")
+    _check(load().mp_adam_step(master.data_ptr(), m.data_ptr(), v.data_ptr(), grad.data_ptr(),
+                               param_bf16.data_ptr(), master.numel(), lr, beta1, beta2, eps,
+                               weight_decay, grad_scale, int(step), _stream(stream)),
+           "mp_adam_step")
+
+
+def cast_f32_bf16(x: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    _check(load().mp_cast_f32_bf16(x.data_ptr(), out.data_ptr(), x.numel(), _stream(stream)),
+           "mp_cast_f32_bf16")
+    return out
+
+
+def cast_bf16_f32(x: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    _check(load().mp_cast_bf16_f32(x.data_ptr(), out.data_ptr(), x.numel(), _stream(stream)),
+           "mp_cast_bf16_f32")
+    return out
+
+
+def accum_bf16_f32(x: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    _check(load().mp_accum_bf16_f32(x.data_ptr(), out.data_ptr(), x.numel(), _stream(stream)),
+           "mp_accum_bf16_f32")
+    return out

@@ -1,0 +1,68 @@
+"""Throughput of the tcgen05 GEMM at the GPT-1.3B per-device shapes,
+next to torch.matmul (cuBLAS) for context.  CUDA-event timing, warm-up, inputs
+reused (these GEMMs are compute-bound; L2 residency does not change the bound)."""
+import json
+import sys
+
+import torch
+
+from paper_2201_12023_b200 import native
+
+SHAPES = [
+    # name, M, N, K, ta, tb
+    ("qkv_fwd", 8192, 2048, 2048, 0, 0),
+    ("mlp_up_fwd", 8192, 8192, 2048, 0, 0),
+    ("mlp_down_fwd", 8192, 2048, 8192, 0, 0),
+    ("mlp_up_dX", 8192, 2048, 8192, 0, 1),
+    ("mlp_up_dW", 2048, 8192, 8192, 1, 0),
+    ("sq4096", 4096, 4096, 4096, 0, 0),
+    ("sq8192", 8192, 8192, 8192, 0, 0),
+]
+
+
+def timeit(fn, iters=20, warm=5):
+    for _ in range(warm):
+        fn()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e-3
+
+
+def main():
+    rows = []
+    for name, M, N, K, ta, tb in SHAPES:
+        a = torch.randn(K, M, device="cuda", dtype=torch.bfloat16).t() if ta else \
+            torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+        b = torch.randn(N, K, device="cuda", dtype=torch.bfloat16).t() if tb else \
+            torch.randn(K, N, device="cuda", dtype=torch.bfloat16)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        t_mp = timeit(lambda: native.gemm(a, b, out))
+        t_cb = timeit(lambda: torch.matmul(a, b, out=out))
+        fl = 2.0 * M * N * K
+        rows.append({"shape": name, "M": M, "N": N, "K": K, "ta": ta, "tb": tb,
+                     "mp_tflops": fl / t_mp / 1e12, "cublas_tflops": fl / t_cb / 1e12,
+                     "mp_us": t_mp * 1e6})
+        print(json.dumps(rows[-1]), flush=True)
+    # batched attention shapes (one 8-seq microbatch, 32 heads)
+    B, H, s, hd = 8, 32, 1024, 64
+    q = torch.randn(B * s, H * hd, device="cuda", dtype=torch.bfloat16)
+    qh = q.view(B, s, H, hd).permute(0, 2, 1, 3)
+    kt = q.view(B, s, H, hd).permute(0, 2, 3, 1)
+    sc = torch.empty(B, H, s, s, device="cuda", dtype=torch.bfloat16)
+    t = timeit(lambda: native.gemm(qh, kt, sc))
+    print(json.dumps({"shape": "scores_bmm", "mp_tflops": 2.0 * B * H * s * s * hd / t / 1e12,
+                      "mp_us": t * 1e6, "hbm_gbs": sc.numel() * 2 / t / 1e9}), flush=True)
+    ctx = torch.empty(B * s, H * hd, device="cuda", dtype=torch.bfloat16)
+    cv = ctx.view(B, s, H, hd).permute(0, 2, 1, 3)
+    t = timeit(lambda: native.gemm(sc, qh, cv))
+    print(json.dumps({"shape": "ctx_bmm", "mp_tflops": 2.0 * B * H * s * s * hd / t / 1e12,
+                      "mp_us": t * 1e6}), flush=True)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

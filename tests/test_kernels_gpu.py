@@ -1,0 +1,180 @@
+"""Numerics of every libmpexec kernel against a plain PyTorch fp32 reference of
+the same op (on the GPU box).  Tolerances are stated per test: bf16 outputs are
+compared with rtol/atol ~1e-2 scaled to the value range; fp32 outputs of the
+tcgen05 GEMM with 2e-3 relative Frobenius error (bf16 inputs, fp32 accumulate)."""
+import math
+
+import pytest
+import torch
+
+from paper_2201_12023_b200 import native
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_err(x, ref):
+    x = x.float()
+    ref = ref.float()
+    return ((x - ref).norm() / ref.norm().clamp_min(1e-30)).item()
+
+
+def rnd(*shape, scale=1.0, dtype=torch.bfloat16):
+    return (torch.randn(*shape, device="cuda") * scale).to(dtype)
+
+
+@pytest.fixture(autouse=True)
+def _seed():
+    torch.manual_seed(0)
+
+
+GEMM_SHAPES = [(128, 256, 64), (256, 512, 128), (384, 256, 1024), (64, 1024, 1024),
+               (1000, 520, 136), (512, 64, 512), (256, 128, 192), (2048, 2048, 2048)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_layouts(M, N, K, ta, tb):
+    a = rnd(K, M).t() if ta else rnd(M, K)
+    b = rnd(N, K).t() if tb else rnd(K, N)
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    native.gemm(a, b, out)
+    ref = a.float() @ b.float()
+    assert rel_err(out, ref) < 2e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 256), (128, 512, 2048)])
+def test_gemm_bf16_out_alpha_beta(M, N, K):
+    a, b = rnd(M, K), rnd(K, N)
+    c0 = rnd(M, N)
+    out = c0.clone()
+    native.gemm(a, b, out, alpha=0.5, beta=1.0)
+    ref = 0.5 * (a.float() @ b.float()) + c0.float()
+    assert rel_err(out, ref) < 1e-2
+    acc = torch.randn(M, N, device="cuda")
+    acc0 = acc.clone()
+    native.gemm(a, b, acc, beta=1.0)
+    assert rel_err(acc, a.float() @ b.float() + acc0) < 2e-3
+
+
+def test_gemm_gelu_epilogue():
+    a, b = rnd(256, 512), rnd(512, 768, scale=0.05)
+    out = torch.empty(256, 768, device="cuda", dtype=torch.bfloat16)
+    native.gemm(a, b, out, gelu=True)
+    ref = torch.nn.functional.gelu(a.float() @ b.float(), approximate="tanh")
+    assert rel_err(out, ref) < 1e-2
+
+
+def test_gemm_batched_head_views():
+    # head split / merge as strided views: q (T, h) -> (B, H, s, hd)
+    B, s, H, hd = 2, 256, 4, 64
+    T, h = B * s, H * hd
+    q, k, v = rnd(T, h), rnd(T, h), rnd(T, h)
+    qh = q.view(B, s, H, hd).permute(0, 2, 1, 3)          # (B,H,s,hd)
+    kt = k.view(B, s, H, hd).permute(0, 2, 3, 1)          # (B,H,hd,s)  K-major B
+    vh = v.view(B, s, H, hd).permute(0, 2, 1, 3)          # (B,H,s,hd)  MN-major B
+    scores = torch.empty(B, H, s, s, device="cuda", dtype=torch.bfloat16)
+    native.gemm(qh, kt, scores)
+    ref = qh.float() @ kt.float()
+    assert rel_err(scores, ref) < 1e-2
+    ctx = torch.empty(T, h, device="cuda", dtype=torch.bfloat16)
+    ctx_v = ctx.view(B, s, H, hd).permute(0, 2, 1, 3)     # write straight into merged layout
+    native.gemm(scores, vh, ctx_v)
+    ref2 = scores.float() @ vh.float()
+    assert rel_err(ctx_v, ref2) < 1e-2
+    # transposed batched operand (dK = Q^T-style)
+    out = torch.empty(B, H, hd, s, device="cuda", dtype=torch.float32)
+    native.gemm(qh.transpose(-1, -2), scores, out)
+    assert rel_err(out, qh.float().transpose(-1, -2) @ scores.float()) < 2e-3
+
+
+def test_gemm_rejects_misaligned():
+    a = rnd(128, 65)[:, :63]
+    b = rnd(63, 128)
+    with pytest.raises(native.NativeError):
+        native.gemm(a, b, torch.empty(128, 128, device="cuda"))
+
+
+def test_elementwise_ops():
+    x = rnd(4096 + 3, scale=2.0)
+    y = native.gelu(x)
+    assert rel_err(y, torch.nn.functional.gelu(x.float(), approximate="tanh")) < 1e-2
+    dy = rnd(4096 + 3)
+    dx = native.gelu_bwd(x, dy)
+    xf = x.float().requires_grad_()
+    torch.nn.functional.gelu(xf, approximate="tanh").backward(dy.float())
+    assert rel_err(dx, xf.grad) < 1e-2
+    z = native.add(x, dy)
+    assert rel_err(z, x.float() + dy.float()) < 1e-2
+    w = native.scale(x, 0.25)
+    assert rel_err(w, 0.25 * x.float()) < 1e-2
+    acc = torch.zeros(1, device="cuda")
+    native.sumsq(x, acc)
+    assert abs(acc.item() - (x.float() ** 2).sum().item()) / (x.float() ** 2).sum().item() < 1e-4
+
+
+@pytest.mark.parametrize("rows,cols", [(512, 1024), (37, 200), (8, 4096)])
+def test_softmax(rows, cols):
+    x = rnd(rows, cols, scale=3.0)
+    s = 1.0 / math.sqrt(64)
+    y = native.softmax(x, s)
+    ref = torch.softmax(s * x.float(), dim=-1)
+    assert rel_err(y, ref) < 1e-2
+    g = rnd(rows, cols)
+    dx = native.softmax_bwd(y, g, s)
+    xf = x.float().requires_grad_()
+    torch.softmax(s * xf, dim=-1).backward(g.float())
+    assert rel_err(dx, xf.grad) < 2e-2
+
+
+def test_softmax_split_rows():
+    rows, cols, parts = 64, 1024, 4
+    s = 0.125
+    x = rnd(rows, cols, scale=3.0)
+    chunks = x.chunk(parts, dim=1)
+    stats = [native.softmax_stats(c.contiguous(), s, torch.empty(rows, 2, device="cuda")) for c in chunks]
+    m = torch.stack([st[:, 0] for st in stats]).max(0).values
+    z = sum(st[:, 1] * torch.exp(st[:, 0] - m) for st in stats)
+    merged = torch.stack([m, z], 1).contiguous()
+    y = torch.cat([native.softmax_apply(c.contiguous(), merged, s) for c in chunks], 1)
+    assert rel_err(y, torch.softmax(s * x.float(), -1)) < 1e-2
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_pack_unpack_box(dtype):
+    t = torch.randn(6, 40, 24, device="cuda").to(dtype)
+    lo, ext = (1, 8, 8), (3, 16, 16)
+    buf = native.pack_box(t, lo, ext)
+    ref = t[1:4, 8:24, 8:24].reshape(-1)
+    assert torch.equal(buf, ref)
+    dst = torch.zeros_like(t)
+    native.unpack_box(buf, dst, lo, ext)
+    assert torch.equal(dst[1:4, 8:24, 8:24], t[1:4, 8:24, 8:24])
+    assert dst.abs().sum() == t[1:4, 8:24, 8:24].abs().float().sum().to(dtype)
+    # non-vectorisable box (odd inner extent) on a transposed view
+    tv = t.transpose(0, 1)
+    buf2 = native.pack_box(tv, (3, 1, 5), (7, 2, 3))
+    assert torch.equal(buf2, tv[3:10, 1:3, 5:8].reshape(-1))
+
+
+def test_adam_step():
+    n = 10007
+    master = torch.randn(n, device="cuda")
+    m = torch.zeros(n, device="cuda")
+    v = torch.zeros(n, device="cuda")
+    g = torch.randn(n, device="cuda")
+    p = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    ref = master.clone().requires_grad_()
+    opt = torch.optim.AdamW([ref], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.0)
+    for step in (1, 2):
+        ref.grad = g.clone()
+        opt.step()
+        native.adam_step(master, m, v, g, p, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8,
+                         weight_decay=0.0, grad_scale=1.0, step=step)
+    assert rel_err(master, ref.detach()) < 1e-5
+    assert rel_err(p, ref.detach()) < 1e-2
+
+
+def test_launch_counter_advances():
+    c0 = native.launch_count()
+    native.gelu(rnd(64))
+    assert native.launch_count() == c0 + 1
