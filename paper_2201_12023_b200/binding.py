@@ -1,0 +1,144 @@
+"""Numeric binding of the reference IR.
+
+The reference IR carries no op semantics (SURVEY §7 hard part 1): ELEMENTWISE has
+no function, RESHAPE need not preserve element counts (graph.py:240-245) and the
+backward graph is a structural mirror (graph.py:317-366).  The executor fixes
+one binding, derived only from graph structure, so any plan of any builder graph
+gets a well-defined computation:
+
+forward (colocate_with is None)
+  input            graph input (one synthetic microbatch)
+  parameter        weight
+  matmul / bmm     y = a @ b                                    (graph.py:187-188)
+  elementwise(a)   softmax(x / sqrt(d)) over the last dim when a is a bmm
+                   output (the attention probabilities, graph.py:300);
+                   tanh-GeLU otherwise (the MLP activation, graph.py:262,308)
+  elementwise(a,b) a + b                                        (residual, graph.py:305,311)
+  reshape 2D->3D   attention head split (T,h) -> (B*H, s, d); when it feeds the
+                   rhs of a bmm whose lhs is also a head split it is the
+                   key-transposed split (B*H, d, s) (graph.py:297-299)
+  reshape 3D->2D   head merge (B*H, s, d) -> (T, h)                (graph.py:302)
+  reshape reversing dims: transpose; same dims: identity
+backward (colocate_with = f)
+  elementwise(out), colocated with out       loss seed dL/dy = y   (L = 1/2 |y|^2)
+  elementwise(g) colocated with unary f       f'(x) * g (GeLU) / softmax backward
+  elementwise(g) colocated with binary f      g (the add's grad, shared by both operands)
+  elementwise(g1, g2)                         g1 + g2 (gradient accumulation, graph.py:328-332)
+  reshape colocated with a matmul/bmm         operand transpose (graph.py:341-352)
+  reshape colocated with a forward reshape r  inverse of r (graph.py:362-365)
+  matmul / bmm                                dX = g @ W^T, dW = x^T @ g (grad_of tags dW)
+The same table is restated independently in oracle/ (the CPU checker).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+from .plan import (Graph, HEAVY, KIND_BMM, KIND_ELEM, KIND_INPUT, KIND_MATMUL, KIND_PARAM,
+                   KIND_RED, KIND_RESHAPE, PlanError)
+
+
+@dataclass(frozen=True)
+class Bound:
+    op: str                       # semantic op code (see module doc)
+    # head geometry for split / merge reshapes: (B, H, s, d)
+    heads: Optional[tuple[int, int, int, int]] = None
+    # node whose forward tensor the op reads besides its inputs (gelu_bwd / softmax_bwd)
+    fwd_ref: Optional[int] = None
+    softmax_scale: float = 1.0
+
+
+def _head_geom(two_d: tuple[int, int], three_d: tuple[int, int, int],
+               transposed: bool) -> tuple[int, int, int, int]:
+    T, h = two_d
+    X, Y, Z = three_d
+    s, d = (Z, Y) if transposed else (Y, Z)
+    if X * s * d != T * h or T % s or h % d:
+        raise PlanError(f"reshape {two_d} <-> {three_d} is not a head split/merge")
+    B, H = T // s, h // d
+    if B * H != X:
+        raise PlanError(f"reshape {two_d} <-> {three_d}: batch*heads mismatch")
+    return (B, H, s, d)
+
+
+def bind(graph: Graph) -> dict[int, Bound]:
+    out: dict[int, Bound] = {}
+    cons = graph.consumers()
+    for n in graph.nodes:
+        fwd = n.colocate_with is None
+        if n.kind == KIND_INPUT:
+            out[n.id] = Bound("input")
+        elif n.kind == KIND_PARAM:
+            out[n.id] = Bound("param")
+        elif n.kind in HEAVY:
+            out[n.id] = Bound("matmul" if n.kind == KIND_MATMUL else "bmm")
+        elif n.kind == KIND_RED:
+            out[n.id] = Bound("reduce_sum" if fwd else "broadcast")
+        elif n.kind == KIND_ELEM:
+            out[n.id] = _bind_elementwise(graph, n, out)
+        elif n.kind == KIND_RESHAPE:
+            out[n.id] = _bind_reshape(graph, n, out, cons)
+        else:
+            raise PlanError(f"node {n.id}: unknown kind {n.kind}")
+    return out
+
+
+def _bind_elementwise(graph: Graph, n, bound: dict[int, Bound]) -> Bound:
+    if n.colocate_with is None:
+        if len(n.inputs) == 1:
+            src = graph[n.inputs[0]]
+            if src.kind == KIND_BMM:
+                d = graph[src.inputs[0]].dims[-1]       # contraction length of q @ k^T
+                return Bound("softmax", softmax_scale=1.0 / float(d) ** 0.5)
+            return Bound("gelu")
+        if len(n.inputs) == 2:
+            return Bound("add")
+        raise PlanError(f"node {n.id}: elementwise of arity {len(n.inputs)} has no binding")
+    f = graph[n.colocate_with]
+    if len(n.inputs) == 1 and n.inputs[0] == n.colocate_with and f.colocate_with is None:
+        return Bound("seed")
+    if len(n.inputs) == 2:
+        return Bound("add")
+    if len(n.inputs) != 1:
+        raise PlanError(f"node {n.id}: backward elementwise arity {len(n.inputs)}")
+    fb = bound[f.id]
+    if fb.op == "gelu":
+        return Bound("gelu_bwd", fwd_ref=f.inputs[0])
+    if fb.op == "softmax":
+        return Bound("softmax_bwd", fwd_ref=f.id, softmax_scale=fb.softmax_scale)
+    if fb.op == "add":
+        return Bound("identity")
+    raise PlanError(f"node {n.id}: no backward binding for forward op {fb.op}")
+
+
+def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
+    src = graph[n.inputs[0]]
+    ind, outd = src.dims, n.dims
+    if n.colocate_with is not None:
+        f = graph[n.colocate_with]
+        if f.kind in HEAVY:
+            return Bound("transpose")
+        if f.kind == KIND_RESHAPE:
+            fb = bound[f.id]
+            inverse = {"split": "merge", "split_t": "merge_t", "merge": "split",
+                       "merge_t": "split_t", "transpose": "transpose", "identity": "identity"}
+            op = inverse[fb.op]
+            return Bound(op, heads=fb.heads)
+        if f.kind == KIND_RED:
+            return Bound("broadcast")
+        raise PlanError(f"node {n.id}: backward reshape colocated with {f.kind}")
+    if len(ind) == 2 and len(outd) == 3:
+        transposed = False
+        for c, slot in cons[n.id]:
+            cn = graph[c]
+            if cn.kind == KIND_BMM and slot == 1 and graph[cn.inputs[0]].kind == KIND_RESHAPE:
+                transposed = True
+        return Bound("split_t" if transposed else "split",
+                     heads=_head_geom(ind, outd, transposed))
+    if len(ind) == 3 and len(outd) == 2:
+        return Bound("merge", heads=_head_geom(outd, ind, False))
+    if ind == outd:
+        return Bound("identity")
+    if len(ind) >= 2 and outd == ind[:-2] + (ind[-1], ind[-2]):
+        return Bound("transpose")
+    raise PlanError(f"node {n.id}: reshape {ind} -> {outd} has no binding")

@@ -1,0 +1,778 @@
+"""The B200 plan executor: the drop-in for the reference's
+`emit_instructions -> simulate` path (reshard.py:347-405, sim.py:91-188).
+
+One process per GPU.  Each rank runs the instruction list of the stage that owns
+its device, in order, for real:
+
+  alloc / free      microbatch activation state (act{i}.{b}) and recv buffers
+  recv / send       cross-mesh Transfers: sender-side box packing (mp_pack_box)
+                    and NCCL P2P over NVLink on a per-boundary communicator,
+                    receiver-side unpacking (mp_unpack_box)        reshard.py:97-157
+  all_gather        the paper's local all-gather over a dst replica group
+  compute fwd/bwd   the stage's ops on its logical mesh: each device runs its
+                    local shard (tcgen05 GEMM / row kernels), inputs resharded
+                    to the algorithm's input specs, k-split partials all-reduced
+  sync              end of step: gradient reduction + fused Adam, barrier
+
+The result mirrors SimResult (makespan, utilization, peak_bytes, events) with
+measured times, plus the step loss and (optionally) the parameter gradients.
+"""
+from __future__ import annotations
+
+import math
+import os
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import native
+from .binding import Bound, bind
+from .comm import Comm
+from .layout import all_local, canonical, matmul_algo, relayout_moves, reshape_required
+from .plan import (ExecPlan, Mesh, PlanError, Spec, box_numel, device_box, load_plan,
+                   local_dims, replicated)
+from .schedule import GPIPE, Instr, Program, build_program
+
+
+class ExecError(RuntimeError):
+    """Executor failure naming rank and instruction (the SimError analogue,
+    sim.py:26)."""
+
+
+@dataclass
+class ExecEvent:
+    stage: int
+    op: str
+    label: str
+    start: float
+    end: float
+
+
+@dataclass
+class ExecResult:
+    makespan: float                               # seconds, measured (max over ranks)
+    utilization: dict[int, float]                 # busy (compute/send/all_gather) / makespan
+    peak_bytes: dict[int, int]                    # per device id (torch allocator peak)
+    events: list[ExecEvent]
+    loss: float                                   # sum over microbatches of 1/2 |y|^2
+    step_times: list[float] = field(default_factory=list)
+    grads: Optional[dict[int, np.ndarray]] = None  # global fp32 parameter gradients
+    params: Optional[dict[int, np.ndarray]] = None
+    outputs: Optional[dict] = None                  # (microbatch, node) -> global forward output
+    gpu_launches: int = 0
+
+
+@dataclass
+class AdamConfig:
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.95
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+
+def _lo(box):
+    return tuple(lo for lo, _ in box)
+
+
+def _ext(box):
+    return tuple(hi - lo for lo, hi in box)
+
+
+def _rel(box, origin):
+    return tuple((lo - o, hi - o) for (lo, hi), o in zip(box, origin))
+
+
+class _Op:
+    __slots__ = ("nid", "op", "bound", "ins", "out_spec", "algo", "grad_direct", "extra")
+
+    def __init__(self, nid, op, bound, ins, out_spec, algo=None):
+        self.nid = nid
+        self.op = op
+        self.bound = bound
+        self.ins = ins                   # list of (producer id, required spec)
+        self.out_spec = out_spec
+        self.algo = algo
+        self.grad_direct = False         # dW accumulated straight into the fp32 grad buffer
+        self.extra = None
+
+
+class StageRunner:
+    """Executes one stage's program on one device."""
+
+    def __init__(self, plan: ExecPlan, program: Program, device_id: int, comm: Comm, *,
+                 seed: int = 0, params: Optional[dict[int, np.ndarray]] = None,
+                 inputs: Optional[Callable[[int, int], np.ndarray]] = None,
+                 adam: Optional[AdamConfig] = None, input_scale: float = 1.0,
+                 host_inputs: bool = False):
+        self.plan = plan
+        self.graph = plan.graph
+        self.program = program
+        self.me = device_id
+        self.comm = comm
+        self.st = plan.stage_of_device(device_id)
+        self.mesh: Mesh = self.st.mesh
+        self.sprog = program.stages[self.st.index]
+        self.bound = bind(plan.graph)
+        self.seed = seed
+        self.adam = adam or AdamConfig()
+        self.inputs_fn = inputs
+        self.host_inputs = host_inputs
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.cons = plan.graph.consumers()
+        self._moves_cache: dict = {}
+        self._compile()
+        self._init_params(params)
+        self.step_count = 0
+        self.vals: dict[int, dict[int, torch.Tensor]] = {}
+        self.cache: dict[int, dict] = {}
+        self.loss_acc = torch.zeros(1, dtype=torch.float32, device=self.dev)
+        self.outputs: dict[int, torch.Tensor] = {}
+        self.keep_outputs = False
+        self._host_input_bufs: dict = {}
+        self.h2d_bytes = 0
+        self.pending_sends: list = []
+        self.input_mode = "host" if host_inputs else ("fn" if inputs is not None else "resident")
+        self._resident_inputs: dict = {}
+
+    # ------------------------------------------------------------------ compile
+    def spec(self, nid: int) -> Spec:
+        return canonical(self.st.spec_of(nid), self.mesh)
+
+    def _compile(self):
+        g = self.graph
+        members = set(self.st.op_ids)
+        self.fwd_ops: list[_Op] = []
+        self.bwd_ops: list[_Op] = []
+        self.param_ids: list[int] = []
+        self.input_ids: list[int] = []
+        for nid in sorted(self.st.op_ids):
+            n = g[nid]
+            b = self.bound[nid]
+            out = self.spec(nid)
+            if b.op == "param":
+                self.param_ids.append(nid)
+                continue
+            if b.op == "input":
+                self.input_ids.append(nid)
+                op = _Op(nid, "input", b, [], out)
+                self.fwd_ops.append(op)
+                continue
+            if b.op in ("matmul", "bmm"):
+                algo = matmul_algo(b.op == "bmm", out, self.mesh)
+                ins = [(n.inputs[0], algo.in_specs[0]), (n.inputs[1], algo.in_specs[1])]
+                op = _Op(nid, b.op, b, ins, out, algo)
+                if n.grad_of is not None:
+                    if self.cons[nid]:
+                        raise ExecError(f"node {nid}: a consumed parameter gradient is not "
+                                        "supported (builders never produce one)")
+                    op.grad_direct = True
+            elif n.kind == "reshape":
+                req = reshape_required(b, out, len(g[n.inputs[0]].dims))
+                op = _Op(nid, b.op, b, [(n.inputs[0], req)], out)
+            elif b.op in ("reduce_sum", "broadcast"):
+                raise ExecError(f"node {nid}: reduction ops are not supported by this executor")
+            else:
+                ins = [(p, out) for p in n.inputs]
+                if b.fwd_ref is not None:
+                    ins.append((b.fwd_ref, out))
+                op = _Op(nid, b.op, b, ins, out)
+            (self.fwd_ops if n.colocate_with is None else self.bwd_ops).append(op)
+        # stage outputs that other stages need
+        self.out_ids = set(self.st.output_specs)
+        self.grad_nodes = {g[n].grad_of: n for n in self.st.op_ids if g[n].grad_of is not None}
+        # fwd output of the graph (for the loss seed / checks)
+        self.seed_ids = [o.nid for o in self.bwd_ops if o.op == "seed"]
+        self.members = members
+
+    # ------------------------------------------------------------------ params
+    def _init_params(self, init: Optional[dict[int, np.ndarray]]):
+        """Resident local shards: fp32 master / Adam m, v / fp32 grad in flat
+        buffers (one fused optimizer launch per step) and the bf16 working copy."""
+        g = self.graph
+        sizes = []
+        for pid in self.param_ids:
+            sizes.append(math.prod(local_dims(g[pid].dims, self.spec(pid), self.mesh)))
+        total = sum(sizes)
+        self.n_param = total
+        self.master = torch.zeros(total, dtype=torch.float32, device=self.dev)
+        self.m = torch.zeros_like(self.master)
+        self.v = torch.zeros_like(self.master)
+        self.gradbuf = torch.zeros_like(self.master)
+        self.wbf16 = torch.zeros(total, dtype=torch.bfloat16, device=self.dev)
+        self.pviews: dict[int, tuple[int, tuple[int, ...]]] = {}
+        off = 0
+        for pid, sz in zip(self.param_ids, sizes):
+            ld = local_dims(g[pid].dims, self.spec(pid), self.mesh)
+            self.pviews[pid] = (off, ld)
+            box = device_box(g[pid].dims, self.spec(pid), self.mesh, self.me)
+            if init is not None:
+                full = np.asarray(init[pid], dtype=np.float32)
+                loc = full[tuple(slice(lo, hi) for lo, hi in box)]
+                self.master[off:off + sz].copy_(torch.from_numpy(np.ascontiguousarray(loc)).reshape(-1))
+            else:
+                gen = torch.Generator(device=self.dev)
+                gen.manual_seed(hash((self.seed, "param", pid)) & 0x7FFFFFFF)
+                fan_in = g[pid].dims[0]
+                full = torch.randn(g[pid].dims, generator=gen, device=self.dev) / math.sqrt(fan_in)
+                loc = full[tuple(slice(lo, hi) for lo, hi in box)]
+                self.master[off:off + sz].copy_(loc.reshape(-1))
+                del full
+            off += sz
+        if total:
+            native.cast_f32_bf16(self.master, self.wbf16)
+        # gradient buffers of grad_of nodes are laid out in the dW node's own spec;
+        # when that differs from the parameter spec a separate fp32 buffer is used.
+        self.gviews: dict[int, torch.Tensor] = {}
+        for pid in self.param_ids:
+            dw = self.grad_nodes.get(pid)
+            off, ld = self.pviews[pid]
+            if dw is None:
+                continue
+            dws = self.spec(dw)
+            if dws == self.spec(pid):
+                self.gviews[dw] = self.gradbuf[off:off + math.prod(ld)].view(ld)
+            else:
+                dld = local_dims(g[dw].dims, dws, self.mesh)
+                self.gviews[dw] = torch.zeros(dld, dtype=torch.float32, device=self.dev)
+
+    def param_view(self, pid: int) -> torch.Tensor:
+        off, ld = self.pviews[pid]
+        return self.wbf16[off:off + math.prod(ld)].view(ld)
+
+    # ------------------------------------------------------------------ values
+    def value(self, mb: int, nid: int) -> torch.Tensor:
+        if nid in self.pviews:
+            return self.param_view(nid)
+        try:
+            return self.vals[mb][nid]
+        except KeyError:
+            raise ExecError(f"rank {self.me}: value of node {nid} for microbatch {mb} "
+                            f"is not available") from None
+
+    def get(self, mb: int, nid: int, req: Spec) -> torch.Tensor:
+        """Local shard of node `nid` in layout `req` (reshard on demand)."""
+        have = self.spec(nid)
+        v = self.value(mb, nid)
+        if req == have:
+            return v
+        key = (nid, req)
+        c = self.cache.setdefault(mb, {})
+        if key in c:
+            return c[key]
+        dims = self.graph[nid].dims
+        if all_local(dims, have, req, self.mesh):
+            mine = device_box(dims, have, self.mesh, self.me)
+            want = device_box(dims, req, self.mesh, self.me)
+            out = self._narrow(v, [(lo - o, hi - lo) for (lo, hi), (o, _) in zip(want, mine)])
+        else:
+            out = self._relayout(self._as3(v), dims, have, req)
+        c[key] = out
+        return out
+
+    def _narrow(self, v: torch.Tensor, cuts) -> torch.Tensor:
+        """Slice a local value by logical (offset, length) per dim; head-split
+        4-D views are narrowed on their batch dim when aligned to heads."""
+        if v.dim() == len(cuts) + 1 and all(c[0] == 0 and c[1] == n
+                                           for c, n in zip(cuts[1:], v.shape[2:])):
+            H = v.shape[1]
+            off, ln = cuts[0]
+            if off % H == 0 and ln % H == 0:
+                return v.narrow(0, off // H, ln // H)
+        if v.dim() != len(cuts):
+            v = self._as3(v)
+        for d, (off, ln) in enumerate(cuts):
+            if off != 0 or ln != v.shape[d]:
+                v = v.narrow(d, off, ln)
+        return v
+
+    def _relayout(self, v: torch.Tensor, dims, have: Spec, req: Spec) -> torch.Tensor:
+        key = (dims, have, req)
+        moves = self._moves_cache.get(key)
+        if moves is None:
+            moves = relayout_moves(dims, have, req, self.mesh)
+            self._moves_cache[key] = moves
+        mine = _lo(device_box(dims, have, self.mesh, self.me))
+        want = _lo(device_box(dims, req, self.mesh, self.me))
+        out = torch.empty(local_dims(dims, req, self.mesh), dtype=v.dtype, device=self.dev)
+        sends, recvs = [], []
+        for mv in moves:
+            if mv.src == self.me and mv.dst == self.me:
+                buf = native.pack_box(v, _lo(_rel(mv.box, mine)), _ext(mv.box))
+                native.unpack_box(buf, out, _lo(_rel(mv.box, want)), _ext(mv.box))
+            elif mv.src == self.me:
+                sends.append((native.pack_box(v, _lo(_rel(mv.box, mine)), _ext(mv.box)), mv.dst))
+            elif mv.dst == self.me:
+                buf = torch.empty(box_numel(mv.box), dtype=v.dtype, device=self.dev)
+                recvs.append((buf, mv.src, mv.box))
+        if sends or recvs:
+            grp = self.comm.stage_group(self.st.index, self.mesh)
+            works = self.comm.p2p(sends, [(b, s) for b, s, _ in recvs], grp)
+            for w in works:
+                w.wait()
+            for buf, _, box in recvs:
+                native.unpack_box(buf, out, _lo(_rel(box, want)), _ext(box))
+        return out
+
+    # ------------------------------------------------------------------ kernels
+    def _contig(self, t: torch.Tensor) -> torch.Tensor:
+        if t.is_contiguous():
+            return t
+        return native.pack_box(t, (0,) * t.dim(), tuple(t.shape)).view(t.shape)
+
+    def _allreduce(self, t: torch.Tensor, axes: tuple[int, ...], op=dist.ReduceOp.SUM):
+        if self.mesh.group_extent(axes) > 1:
+            self.comm.all_reduce(t, self.comm.axis_group(self.st.index, self.mesh, axes, self.me), op)
+
+    def _gemm_operands(self, a, b):
+        """Bring two (possibly head-split 4-D) operands to a common batch form."""
+        if a.dim() == b.dim():
+            return a, b
+        if a.dim() == 4 and b.dim() == 3:
+            return a, self._contig(b).view(a.shape[0], a.shape[1], *b.shape[1:])
+        if a.dim() == 3 and b.dim() == 4:
+            return self._contig(a).view(b.shape[0], b.shape[1], *a.shape[1:]), b
+        raise ExecError(f"gemm operand ranks {a.dim()} / {b.dim()}")
+
+    def _run_matmul(self, mb: int, op: _Op) -> Optional[torch.Tensor]:
+        a = self.get(mb, op.ins[0][0], op.ins[0][1])
+        b = self.get(mb, op.ins[1][0], op.ins[1][1])
+        a, b = self._gemm_operands(a, b)
+        k_axes = op.algo.k_axes
+        if op.grad_direct:
+            gv = self.gviews[op.nid]
+            out_view = gv if a.dim() == 2 else gv.view(*a.shape[:-2], a.shape[-2], b.shape[-1])
+            self._gemm(a, b, out_view, beta=1.0)
+            return None
+        shape = tuple(a.shape[:-2]) + (a.shape[-2], b.shape[-1])
+        out = torch.empty(shape, dtype=torch.bfloat16, device=self.dev)
+        self._gemm(a, b, out)
+        if k_axes:
+            self._allreduce(out, k_axes)
+        if out.dim() == 4:
+            out = out.view(out.shape[0] * out.shape[1], *out.shape[2:])
+        return out
+
+    def _gemm(self, a, b, out, beta=0.0):
+        if out.stride(-1) != 1 and out.stride(-2) == 1:
+            native.gemm(b.transpose(-1, -2), a.transpose(-1, -2), out.transpose(-1, -2), beta=beta)
+        else:
+            native.gemm(a, b, out, beta=beta)
+
+    def _run_reshape(self, mb: int, op: _Op) -> torch.Tensor:
+        x = self.get(mb, op.ins[0][0], op.ins[0][1])
+        kind = op.op
+        if kind == "identity":
+            y = x
+        elif kind == "transpose":
+            y = x.transpose(-1, -2)
+        else:
+            B, H, s, d = op.bound.heads
+            if kind == "split":            # (T,h) -> (B,H,s,d)
+                y = self._contig(x).view(B, s, H, d).permute(0, 2, 1, 3)
+            elif kind == "split_t":        # (T,h) -> (B,H,d,s)
+                y = self._contig(x).view(B, s, H, d).permute(0, 2, 3, 1)
+            elif kind in ("merge", "merge_t"):
+                x4 = x if x.dim() == 4 else self._contig(x).view(B, H, *x.shape[1:])
+                perm = (0, 2, 1, 3) if kind == "merge" else (0, 3, 1, 2)
+                y = self._contig(x4.permute(*perm)).view(B * s, H * d)
+            else:
+                raise ExecError(f"reshape op {kind}")
+        if not op.out_spec.is_replicated() and kind not in ("identity", "transpose"):
+            box = device_box(self.graph[op.nid].dims, op.out_spec, self.mesh, self.me)
+            y = self._contig(y) if y.dim() == len(box) else self._contig(y).view(
+                *self.graph[op.nid].dims)
+            for d, (lo, hi) in enumerate(box):
+                y = y.narrow(d, lo, hi - lo)
+        return y
+
+    def _split_axes(self, op: _Op) -> tuple[int, ...]:
+        return tuple(a for a in op.out_spec.dims[-1] if self.mesh.extent(a) > 1)
+
+    def _as3(self, t: torch.Tensor) -> torch.Tensor:
+        return t if t.dim() != 4 else self._contig(t).view(-1, *t.shape[2:])
+
+    def _run_elementwise(self, mb: int, op: _Op) -> torch.Tensor:
+        k = op.op
+        xs = [self._contig(self._as3(self.get(mb, p, r))) for p, r in op.ins]
+        if k == "gelu":
+            return native.gelu(xs[0])
+        if k == "add":
+            return native.add(xs[0], xs[1])
+        if k == "identity":
+            return xs[0]
+        if k == "seed":
+            y = xs[0]
+            if self._is_representative(op.nid):
+                native.sumsq(y, self.loss_acc)
+            if self.keep_outputs:
+                self.outputs[mb] = y.float().clone()
+            return y
+        if k == "gelu_bwd":
+            g, x = xs
+            return native.gelu_bwd(x, g)
+        if k == "softmax":
+            x = xs[0]
+            split = self._split_axes(op)
+            s = op.bound.softmax_scale
+            if not split:
+                return native.softmax(x, s)
+            rows = x.numel() // x.shape[-1]
+            stats = native.softmax_stats(x, s, torch.empty(rows, 2, dtype=torch.float32, device=self.dev))
+            mx = stats[:, 0].contiguous()
+            self._allreduce(mx, split, dist.ReduceOp.MAX)
+            z = (stats[:, 1] * torch.exp(stats[:, 0] - mx)).contiguous()
+            self._allreduce(z, split)
+            merged = torch.stack([mx, z], 1).contiguous()
+            return native.softmax_apply(x, merged, s)
+        if k == "softmax_bwd":
+            g, y = xs
+            split = self._split_axes(op)
+            s = op.bound.softmax_scale
+            if not split:
+                return native.softmax_bwd(y, g, s)
+            rows = y.numel() // y.shape[-1]
+            rd = native.softmax_rowdot(y, g, torch.empty(rows, dtype=torch.float32, device=self.dev))
+            self._allreduce(rd, split)
+            return native.softmax_bwd(y, g, s, rowdot=rd)
+        raise ExecError(f"node {op.nid}: no kernel for elementwise op {k}")
+
+    def _is_representative(self, nid: int) -> bool:
+        """True on exactly one device per replica group of nid's spec."""
+        i, j = self.mesh.coords(self.me)
+        rep = set(self.spec(nid).replicated_axes())
+        return (0 not in rep or i == 0) and (1 not in rep or j == 0)
+
+    def _load_input(self, mb: int, op: _Op) -> torch.Tensor:
+        """One microbatch of a graph input, local shard per its spec.
+        fn: caller-provided global arrays (tests / oracle parity);
+        resident: synthetic N(0,1) kept in HBM (two alternating microbatches);
+        host: the same from pinned host memory, copied H2D every microbatch."""
+        g = self.graph
+        dims = g[op.nid].dims
+        box = device_box(dims, op.out_spec, self.mesh, self.me)
+        sl = tuple(slice(lo, hi) for lo, hi in box)
+        if self.input_mode == "fn":
+            full = np.asarray(self.inputs_fn(mb, op.nid), dtype=np.float32)
+            return torch.from_numpy(np.ascontiguousarray(full[sl])).to(
+                self.dev, dtype=torch.bfloat16)
+        key = (op.nid, mb % 2)
+        if self.input_mode == "host":
+            hb = self._host_input_bufs.get(key)
+            if hb is None:
+                gen = torch.Generator()
+                gen.manual_seed(hash((self.seed, "input", op.nid, mb % 2)) & 0x7FFFFFFF)
+                full = torch.randn(dims, generator=gen)
+                hb = full[sl].contiguous().to(torch.bfloat16).pin_memory()
+                self._host_input_bufs[key] = hb
+            self.h2d_bytes += hb.numel() * hb.element_size()
+            return hb.to(self.dev, non_blocking=True)
+        t = self._resident_inputs.get(key)
+        if t is None:
+            gen = torch.Generator(device=self.dev)
+            gen.manual_seed(hash((self.seed, "input", op.nid, mb % 2)) & 0x7FFFFFFF)
+            full = torch.randn(dims, generator=gen, device=self.dev, dtype=torch.float32)
+            t = full[sl].to(torch.bfloat16).contiguous()
+            self._resident_inputs[key] = t
+        return t
+
+    # ------------------------------------------------------------------ phases
+    def compute(self, phase: str, mb: int):
+        vals = self.vals.setdefault(mb, {})
+        for op in (self.fwd_ops if phase == "fwd" else self.bwd_ops):
+            try:
+                if op.op == "input":
+                    out = self._load_input(mb, op)
+                elif op.op in ("matmul", "bmm"):
+                    out = self._run_matmul(mb, op)
+                elif self.graph[op.nid].kind == "reshape":
+                    out = self._run_reshape(mb, op)
+                else:
+                    out = self._run_elementwise(mb, op)
+            except native.NativeError as e:
+                raise ExecError(f"rank {self.me} stage {self.st.index} {phase}{mb} node "
+                                f"{op.nid} ({op.op}): {e}") from None
+            if out is not None:
+                vals[op.nid] = out
+
+    def recv(self, ins: Instr):
+        bd = ins.boundary
+        mb = ins.microbatch
+        vals = self.vals.setdefault(mb, {})
+        recvs = []
+        for bt in bd.tensors:
+            node = self.graph[bt.node]
+            dspec = canonical(bt.dst_spec, self.mesh)
+            mine = device_box(node.dims, dspec, self.mesh, self.me)
+            out = torch.empty(local_dims(node.dims, dspec, self.mesh), dtype=torch.bfloat16,
+                              device=self.dev)
+            vals[bt.node] = out
+            for t in bt.xplan.transfers:
+                if t.dst_device == self.me:
+                    buf = torch.empty(box_numel(t.box), dtype=torch.bfloat16, device=self.dev)
+                    recvs.append((buf, t.src_device, out, _lo(_rel(t.box, _lo(mine))), _ext(t.box)))
+        if recvs:
+            works = self.comm.p2p([], [(b, s) for b, s, *_ in recvs],
+                                  self.comm.boundary_group(bd, self.plan))
+            for w in works:
+                w.wait()
+            for buf, _, out, lo, ext in recvs:
+                native.unpack_box(buf, out, lo, ext)
+
+    def all_gather(self, ins: Instr):
+        bd = ins.boundary
+        mb = ins.microbatch
+        gidx = ins.gather_index
+        # locate the tensor owning the gather_index-th gather of this boundary
+        k = gidx
+        for bt in bd.tensors:
+            if k < len(bt.xplan.gathers):
+                ga = bt.xplan.gathers[k]
+                break
+            k -= len(bt.xplan.gathers)
+        if self.me not in ga.devices:
+            return
+        out = self.vals[mb][bt.node]
+        tile_lo = ga.box[0][0]
+        rows = [p[0][1] - p[0][0] for p in ga.pieces]
+        g = len(ga.devices)
+        r = ga.devices.index(self.me)
+        grp = self.comm.gather_group(bd, ga.devices)
+        flat = out.view(-1)
+        row_elems = out.numel() // out.shape[0]
+        if all(x == rows[0] for x in rows):
+            n = rows[0] * row_elems
+            self.comm.all_gather_into(flat, flat[r * n:(r + 1) * n], grp)
+        else:
+            sends, recvs = [], []
+            starts = [p[0][0] - tile_lo for p in ga.pieces]
+            mine = flat[starts[r] * row_elems:(starts[r] + rows[r]) * row_elems]
+            for q, dev in enumerate(ga.devices):
+                if q == r:
+                    continue
+                if rows[r]:
+                    sends.append((mine, dev))
+                if rows[q]:
+                    recvs.append((flat[starts[q] * row_elems:(starts[q] + rows[q]) * row_elems], dev))
+            for w in self.comm.p2p(sends, recvs, grp):
+                w.wait()
+
+    def send(self, ins: Instr):
+        bd = ins.boundary
+        mb = ins.microbatch
+        sends = []
+        for bt in bd.tensors:
+            node = self.graph[bt.node]
+            v = self._as3(self.value(mb, bt.node))
+            mine = _lo(device_box(node.dims, self.spec(bt.node), self.mesh, self.me))
+            for t in bt.xplan.transfers:
+                if t.src_device == self.me:
+                    sends.append((native.pack_box(v, _lo(_rel(t.box, mine)), _ext(t.box)),
+                                  t.dst_device))
+        if sends:
+            self.pending_sends += self.comm.p2p(sends, [], self.comm.boundary_group(bd, self.plan))
+
+    def free(self, ins: Instr):
+        if ins.buffer and ins.buffer.startswith("act"):
+            self.vals.pop(ins.microbatch, None)
+            self.cache.pop(ins.microbatch, None)
+
+    # ------------------------------------------------------------------ optimizer
+    def reduce_grads(self):
+        """Finish the gradient of every parameter: all-reduce the k-split partial
+        sums accumulated over the microbatches (sharding.py:284-291; one reduction
+        per step instead of per microbatch, the sum is linear) and move them to
+        the parameter's layout."""
+        g = self.graph
+        for pid in self.param_ids:
+            dw = self.grad_nodes.get(pid)
+            if dw is None:
+                continue
+            gv = self.gviews[dw]
+            algo = matmul_algo(self.bound[dw].op == "bmm", self.spec(dw), self.mesh)
+            if algo.k_axes:
+                self._allreduce(gv, algo.k_axes)
+            if self.spec(dw) != self.spec(pid):
+                off, ld = self.pviews[pid]
+                moved = self._relayout(gv, g[dw].dims, self.spec(dw), self.spec(pid))
+                native.pack_box(moved, (0,) * moved.dim(), tuple(moved.shape),
+                                out=self.gradbuf[off:off + math.prod(ld)])
+
+    def apply_update(self):
+        self.step_count += 1
+        if self.n_param:
+            a = self.adam
+            native.adam_step(self.master, self.m, self.v, self.gradbuf, self.wbf16, lr=a.lr,
+                             beta1=a.beta1, beta2=a.beta2, eps=a.eps,
+                             weight_decay=a.weight_decay, grad_scale=1.0, step=self.step_count)
+
+    def optimizer_step(self):
+        self.reduce_grads()
+        self.apply_update()
+
+    def zero_grads(self):
+        self.gradbuf.zero_()
+        for dw, gv in self.gviews.items():
+            if gv.data_ptr() < self.gradbuf.data_ptr() or \
+                    gv.data_ptr() >= self.gradbuf.data_ptr() + self.gradbuf.numel() * 4:
+                gv.zero_()
+
+    def local_grad(self, pid: int) -> torch.Tensor:
+        off, ld = self.pviews[pid]
+        return self.gradbuf[off:off + math.prod(ld)].view(ld)
+
+    # ------------------------------------------------------------------ step
+    def run_step(self, *, record: bool = False, update: bool = True):
+        """Run the stage's instruction list once; returns measured events."""
+        self.zero_grads()
+        self.loss_acc.zero_()
+        events = []
+        stream = torch.cuda.current_stream()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for ins in self.sprog.instructions:
+            if record and ins.op in ("compute", "send", "recv", "all_gather"):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            if ins.op == "compute":
+                self.compute(ins.phase, ins.microbatch)
+            elif ins.op == "recv":
+                self.recv(ins)
+            elif ins.op == "send":
+                self.send(ins)
+            elif ins.op == "all_gather":
+                self.all_gather(ins)
+            elif ins.op == "free":
+                self.free(ins)
+            elif ins.op == "sync":
+                for w in self.pending_sends:
+                    w.wait()
+                self.pending_sends = []
+                if update:
+                    self.optimizer_step()
+            if record and ins.op in ("compute", "send", "recv", "all_gather"):
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                events.append((ins, e0, e1))
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record(stream)
+        return t0, t1, events
+
+
+def _label(ins: Instr) -> str:
+    if ins.op == "compute":
+        return f"{ins.phase}{ins.microbatch}@{ins.stage}"
+    if ins.op in ("send", "recv"):
+        return ins.tag or ins.op
+    return ins.op
+
+
+def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, steps: int = 1,
+            params: Optional[dict[int, np.ndarray]] = None,
+            inputs: Optional[Callable[[int, int], np.ndarray]] = None,
+            seed: int = 0, adam: Optional[AdamConfig] = None, record: bool = True,
+            collect: bool = False, update: bool = True) -> ExecResult:
+    """Run `steps` training steps of a reference plan on this process's GPU.
+
+    Call on every rank (RANK/WORLD_SIZE from torch.distributed, rank = device
+    id).  `params` / `inputs` (global fp32 arrays, identical on every rank) make
+    runs reproducible against the CPU oracle; by default weights and inputs are
+    synthetic (seeded).  With collect=True the result carries global parameter
+    gradients of the last step (before the update) and the forward outputs."""
+    if not torch.cuda.is_available():
+        raise ExecError("execute needs a CUDA device; there is no CPU execution path")
+    native.load()
+    plan = plan if isinstance(plan, ExecPlan) else load_plan(plan)
+    program = program or build_program(plan, schedule)
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    if world != plan.num_devices:
+        raise ExecError(f"plan needs {plan.num_devices} devices, running on {world}")
+    comm = Comm(plan, program, rank, world)
+    runner = StageRunner(plan, program, rank, comm, seed=seed, params=params, inputs=inputs,
+                         adam=adam)
+    runner.keep_outputs = collect
+    launches0 = native.launch_count()
+    step_times = []
+    last_events = []
+    grads = None
+    for step in range(steps):
+        last = step == steps - 1
+        if world > 1:
+            dist.barrier(group=comm.world_group)
+        torch.cuda.synchronize()
+        t0, t1, evs = runner.run_step(record=record and last, update=update and not (collect and last))
+        torch.cuda.synchronize()
+        step_times.append(t0.elapsed_time(t1) * 1e-3)
+        if last:
+            last_events = [(ins, t0.elapsed_time(a) * 1e-3, t0.elapsed_time(b) * 1e-3)
+                           for ins, a, b in evs]
+            if collect:
+                runner.reduce_grads()
+                grads = _collect_grads(runner, comm, world)
+                if update:
+                    runner.apply_update()
+    loss = runner.loss_acc.clone()
+    if world > 1:
+        dist.all_reduce(loss, group=comm.world_group)
+    times = torch.tensor(step_times, dtype=torch.float64)
+    if world > 1:
+        tt = times.cuda()
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=comm.world_group)
+        times = tt.cpu()
+    makespan = float(times[-1])
+    events = [ExecEvent(ins.stage, ins.op, _label(ins), s, e) for ins, s, e in last_events]
+    busy = sum(e - s for ins, s, e in last_events if ins.op in ("compute", "send", "all_gather"))
+    util = {runner.st.index: busy / makespan if makespan > 0 else 0.0}
+    peak = {rank: int(torch.cuda.max_memory_allocated())}
+    outputs = None
+    if collect:
+        outputs = _collect_outputs(runner, comm, world)
+    return ExecResult(makespan=makespan, utilization=util, peak_bytes=peak, events=events,
+                      loss=0.5 * float(loss.item()), step_times=[float(x) for x in times],
+                      grads=grads, outputs=outputs,
+                      gpu_launches=native.launch_count() - launches0)
+
+
+def _gather_global(runner: StageRunner, comm: Comm, world: int, items: dict) -> dict:
+    """items: key -> (global dims, local fp32 tensor, global box) on this rank.
+    Returns key -> assembled global np array (on every rank)."""
+    local = {k: (dims, t.detach().float().cpu().numpy(), box) for k, (dims, t, box) in items.items()}
+    allparts = [local]
+    if world > 1:
+        allparts = [None] * world
+        dist.all_gather_object(allparts, local, group=comm.world_group)
+    out: dict = {}
+    for part in allparts:
+        for k, (dims, arr, box) in part.items():
+            if k not in out:
+                out[k] = np.zeros(dims, dtype=np.float32)
+            out[k][tuple(slice(lo, hi) for lo, hi in box)] = arr
+    return out
+
+
+def _collect_grads(runner: StageRunner, comm: Comm, world: int) -> dict[int, np.ndarray]:
+    """Global parameter gradients after reduce_grads (before the update)."""
+    g = runner.graph
+    items = {}
+    for pid in runner.param_ids:
+        if runner.grad_nodes.get(pid) is None:
+            continue
+        box = device_box(g[pid].dims, runner.spec(pid), runner.mesh, runner.me)
+        items[pid] = (g[pid].dims, runner.local_grad(pid), box)
+    return _gather_global(runner, comm, world, items)
+
+
+def _collect_outputs(runner: StageRunner, comm: Comm, world: int) -> dict[int, np.ndarray]:
+    items = {}
+    for sid in runner.seed_ids:
+        y = runner.graph[sid].inputs[0]
+        dims = runner.graph[y].dims
+        box = device_box(dims, runner.spec(sid), runner.mesh, runner.me)
+        for mb, t in runner.outputs.items():
+            items[(mb, y)] = (dims, t.view(*[hi - lo for lo, hi in box]), box)
+    return _gather_global(runner, comm, world, items)

@@ -1,0 +1,47 @@
+"""GPU executor parity against the CPU oracle (tolerances in parity_harness.TOL).
+
+Single-device plans run in-process; multi-device plans are launched with
+torchrun when the box has enough GPUs (gpurun --gpus N), else skipped."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+from parity_harness import ROOT, TOL, run_plan
+
+pytestmark = pytest.mark.gpu
+
+SINGLE = ["plans/mlp_n1/plan.json", "plans/tiny_gpt_n1/plan.json"]
+MULTI = [("plans/mlp_n2/plan.json", 2), ("plans/tiny_gpt_n2/plan.json", 2),
+         ("plans/tiny_gpt_n4/plan.json", 4), ("plans/cfg1/plan.json", 4),
+         ("plans/tiny_gpt_n8/plan.json", 8)]
+
+
+@pytest.mark.parametrize("plan", SINGLE)
+@pytest.mark.parametrize("schedule", ["1f1b", "gpipe"])
+def test_single_device_parity(plan, schedule):
+    errs = run_plan(ROOT / plan, schedule)
+    print(json.dumps(errs))
+    assert errs["loss"] <= TOL["loss"], errs
+    assert errs["output"] <= TOL["output"], errs
+    assert errs["grad"] <= TOL["grad"], errs
+    assert errs["gpu_launches"] > 0
+
+
+@pytest.mark.parametrize("plan,n", MULTI)
+def test_multi_device_parity(plan, n):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29400 + n),
+           str(ROOT / "scripts/parity_run.py"), str(ROOT / plan)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "PYTHONPATH": str(ROOT)})
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
+    errs = json.loads(lines[-1])
+    assert errs["ok"], errs
