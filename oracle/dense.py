@@ -66,8 +66,8 @@ def eval_node(code, info, n, args, val):
     return reshape_op(code, info, args[0])
 
 
-def run(plan_doc, params, inputs, num_microbatches):
-    """-> (loss, grads{param id: array}, outputs{mb: array}) in float64."""
+def run(plan_doc, params, inputs, num_microbatches, dtype=np.float64):
+    """-> (loss, grads{param id: array}, outputs{mb: array}) in `dtype`."""
     doc, nodes, _ = ir.load(plan_doc)
     bound = ir.bind(nodes)
     grads = {}
@@ -79,10 +79,10 @@ def run(plan_doc, params, inputs, num_microbatches):
             nid = n["id"]
             code, info = bound[nid]
             if code == "input":
-                val[nid] = np.asarray(inputs(mb, nid), dtype=np.float64)
+                val[nid] = np.asarray(inputs(mb, nid), dtype=dtype)
                 continue
             if code == "parameter":
-                val[nid] = np.asarray(params[nid], dtype=np.float64)
+                val[nid] = np.asarray(params[nid], dtype=dtype)
                 continue
             args = [val[p] for p in ir.node_inputs(n)]
             val[nid] = eval_node(code, info, n, args, val)

@@ -123,6 +123,11 @@ def _split_batch(t: torch.Tensor, name: str):
     return [r, c, rs, cs, t.stride(0), t.stride(1)], (t.shape[0], t.shape[1])
 
 
+# Optional per-launch timing of the GEMM (bench.py roofline): list of
+# (flops, start_event, end_event) recorded on the launching stream.
+gemm_timer: Optional[list] = None
+
+
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 1.0,
          beta: float = 0.0, gelu: bool = False, stream=None) -> torch.Tensor:
     """out = alpha * a @ b + beta * out on the tcgen05 kernel.  a: (…, M, K),
@@ -137,10 +142,19 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
     cd, cb = _split_batch(out, "out")
     if not (ab == bb == cb):
         raise NativeError(f"batch mismatch {ab} {bb} {cb}")
+    st = _stream(stream)
+    timer = gemm_timer
+    if timer is not None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
     rc = load().mp_gemm_bf16(a.data_ptr(), _arr(ad), b.data_ptr(), _arr(bd), out.data_ptr(),
                              _arr(cd), 1 if out.dtype == torch.float32 else 0, ab[0], ab[1],
-                             float(alpha), float(beta), 1 if gelu else 0, _stream(stream))
+                             float(alpha), float(beta), 1 if gelu else 0, st)
     _check(rc, "mp_gemm_bf16")
+    if timer is not None:
+        e1.record()
+        timer.append((2.0 * ad[0] * ad[1] * bd[1] * ab[0] * ab[1], e0, e1))
     return out
 
 

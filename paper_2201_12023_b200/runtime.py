@@ -671,6 +671,75 @@ def _label(ins: Instr) -> str:
     return ins.op
 
 
+class Executor:
+    """Public API: one rank's executor for a reference plan.
+
+        ex = Executor("plan.json", schedule="1f1b")
+        stats = ex.step()            # one training step (all microbatches + update)
+        res = ex.result()            # SimResult-shaped summary of the last step
+
+    Call on every rank (rank = device id of the (1,N) cluster)."""
+
+    def __init__(self, plan, program: Optional[Program] = None, *, schedule: str = GPIPE,
+                 params: Optional[dict[int, np.ndarray]] = None,
+                 inputs: Optional[Callable[[int, int], np.ndarray]] = None, seed: int = 0,
+                 adam: Optional[AdamConfig] = None, host_inputs: bool = False):
+        if not torch.cuda.is_available():
+            raise ExecError("the executor needs a CUDA device; there is no CPU execution path")
+        native.load()
+        self.plan = plan if isinstance(plan, ExecPlan) else load_plan(plan)
+        self.program = program or build_program(self.plan, schedule)
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        if self.world != self.plan.num_devices:
+            raise ExecError(f"plan needs {self.plan.num_devices} devices, running on {self.world}")
+        self.comm = Comm(self.plan, self.program, self.rank, self.world)
+        self.runner = StageRunner(self.plan, self.program, self.rank, self.comm, seed=seed,
+                                  params=params, inputs=inputs, adam=adam,
+                                  host_inputs=host_inputs)
+        self.step_times: list[float] = []
+        self.last_events: list = []
+
+    def barrier(self):
+        if self.world > 1:
+            dist.barrier(group=self.comm.world_group)
+
+    def step(self, *, record: bool = False, update: bool = True) -> float:
+        """One step; returns this rank's device time (seconds)."""
+        t0, t1, evs = self.runner.run_step(record=record, update=update)
+        torch.cuda.synchronize()
+        dt = t0.elapsed_time(t1) * 1e-3
+        self.step_times.append(dt)
+        if record:
+            self.last_events = [(ins, t0.elapsed_time(a) * 1e-3, t0.elapsed_time(b) * 1e-3)
+                                for ins, a, b in evs]
+        return dt
+
+    def loss(self) -> float:
+        loss = self.runner.loss_acc.clone()
+        if self.world > 1:
+            dist.all_reduce(loss, group=self.comm.world_group)
+        return 0.5 * float(loss.item())
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=self.runner.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.comm.world_group)
+        return float(t.item())
+
+    def result(self, grads=None, outputs=None, launches: int = 0) -> ExecResult:
+        makespan = self.max_over_ranks(self.step_times[-1]) if self.step_times else 0.0
+        evs = self.last_events
+        events = [ExecEvent(ins.stage, ins.op, _label(ins), s, e) for ins, s, e in evs]
+        busy = sum(e - s for ins, s, e in evs if ins.op in ("compute", "send", "all_gather"))
+        util = {self.runner.st.index: busy / makespan if makespan > 0 else 0.0}
+        peak = {self.rank: int(torch.cuda.max_memory_allocated())}
+        return ExecResult(makespan=makespan, utilization=util, peak_bytes=peak, events=events,
+                          loss=self.loss(), step_times=list(self.step_times), grads=grads,
+                          outputs=outputs, gpu_launches=launches)
+
+
 def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, steps: int = 1,
             params: Optional[dict[int, np.ndarray]] = None,
             inputs: Optional[Callable[[int, int], np.ndarray]] = None,
@@ -678,64 +747,29 @@ def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, s
             collect: bool = False, update: bool = True) -> ExecResult:
     """Run `steps` training steps of a reference plan on this process's GPU.
 
-    Call on every rank (RANK/WORLD_SIZE from torch.distributed, rank = device
-    id).  `params` / `inputs` (global fp32 arrays, identical on every rank) make
-    runs reproducible against the CPU oracle; by default weights and inputs are
-    synthetic (seeded).  With collect=True the result carries global parameter
-    gradients of the last step (before the update) and the forward outputs."""
-    if not torch.cuda.is_available():
-        raise ExecError("execute needs a CUDA device; there is no CPU execution path")
-    native.load()
-    plan = plan if isinstance(plan, ExecPlan) else load_plan(plan)
-    program = program or build_program(plan, schedule)
-    rank = dist.get_rank() if dist.is_initialized() else 0
-    world = dist.get_world_size() if dist.is_initialized() else 1
-    if world != plan.num_devices:
-        raise ExecError(f"plan needs {plan.num_devices} devices, running on {world}")
-    comm = Comm(plan, program, rank, world)
-    runner = StageRunner(plan, program, rank, comm, seed=seed, params=params, inputs=inputs,
-                         adam=adam)
-    runner.keep_outputs = collect
+    The drop-in for `simulate(emit_instructions(plan, schedule), ...)`: call on
+    every rank (torch.distributed initialised, rank = device id).  `params` /
+    `inputs` (global fp32 arrays, identical on every rank) make runs reproducible
+    against the CPU oracle; by default weights and inputs are synthetic (seeded).
+    With collect=True the result carries the global parameter gradients of the
+    last step (before its update) and the forward outputs."""
+    ex = Executor(plan, program, schedule=schedule, params=params, inputs=inputs, seed=seed,
+                  adam=adam)
+    ex.runner.keep_outputs = collect
     launches0 = native.launch_count()
-    step_times = []
-    last_events = []
     grads = None
     for step in range(steps):
         last = step == steps - 1
-        if world > 1:
-            dist.barrier(group=comm.world_group)
+        ex.barrier()
         torch.cuda.synchronize()
-        t0, t1, evs = runner.run_step(record=record and last, update=update and not (collect and last))
-        torch.cuda.synchronize()
-        step_times.append(t0.elapsed_time(t1) * 1e-3)
-        if last:
-            last_events = [(ins, t0.elapsed_time(a) * 1e-3, t0.elapsed_time(b) * 1e-3)
-                           for ins, a, b in evs]
-            if collect:
-                runner.reduce_grads()
-                grads = _collect_grads(runner, comm, world)
-                if update:
-                    runner.apply_update()
-    loss = runner.loss_acc.clone()
-    if world > 1:
-        dist.all_reduce(loss, group=comm.world_group)
-    times = torch.tensor(step_times, dtype=torch.float64)
-    if world > 1:
-        tt = times.cuda()
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=comm.world_group)
-        times = tt.cpu()
-    makespan = float(times[-1])
-    events = [ExecEvent(ins.stage, ins.op, _label(ins), s, e) for ins, s, e in last_events]
-    busy = sum(e - s for ins, s, e in last_events if ins.op in ("compute", "send", "all_gather"))
-    util = {runner.st.index: busy / makespan if makespan > 0 else 0.0}
-    peak = {rank: int(torch.cuda.max_memory_allocated())}
-    outputs = None
-    if collect:
-        outputs = _collect_outputs(runner, comm, world)
-    return ExecResult(makespan=makespan, utilization=util, peak_bytes=peak, events=events,
-                      loss=0.5 * float(loss.item()), step_times=[float(x) for x in times],
-                      grads=grads, outputs=outputs,
-                      gpu_launches=native.launch_count() - launches0)
+        ex.step(record=record and last, update=update and not (collect and last))
+        if last and collect:
+            ex.runner.reduce_grads()
+            grads = _collect_grads(ex.runner, ex.comm, ex.world)
+            if update:
+                ex.runner.apply_update()
+    outputs = _collect_outputs(ex.runner, ex.comm, ex.world) if collect else None
+    return ex.result(grads=grads, outputs=outputs, launches=native.launch_count() - launches0)
 
 
 def _gather_global(runner: StageRunner, comm: Comm, world: int, items: dict) -> dict:
