@@ -173,6 +173,7 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 }
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  if (fabsf(x) > 16.f) return x > 0.f ? 1.f : 0.f;  // saturated; avoids 0*inf
   float x2 = x * x;
   float u = k0 * (x + k1 * x2 * x);
   float t = tanhf(u);

@@ -120,6 +120,7 @@ class StageRunner:
         self.bound = bind(plan.graph)
         self.seed = seed
         self.adam = adam or AdamConfig()
+        self.init_std = 0.02
         self.inputs_fn = inputs
         self.host_inputs = host_inputs
         self.dev = torch.device("cuda", torch.cuda.current_device())
@@ -182,6 +183,17 @@ class StageRunner:
                     ins.append((b.fwd_ref, out))
                 op = _Op(nid, b.op, b, ins, out)
             (self.fwd_ops if n.colocate_with is None else self.bwd_ops).append(op)
+        # bmm outputs consumed only by a head merge are written in merged layout
+        for op in self.fwd_ops + self.bwd_ops:
+            if op.op != "bmm" or op.nid in self.st.output_specs:
+                continue
+            users = self.cons[op.nid]
+            if len(users) != 1 or users[0][0] not in members:
+                continue
+            ub = self.bound[users[0][0]]
+            if ub.op in ("merge", "merge_t") and op.out_spec.is_replicated() and \
+                    self.spec(users[0][0]).is_replicated():
+                op.extra = (ub.op, ub.heads)
         # stage outputs that other stages need
         self.out_ids = set(self.st.output_specs)
         self.grad_nodes = {g[n].grad_of: n for n in self.st.op_ids if g[n].grad_of is not None}
@@ -217,8 +229,8 @@ class StageRunner:
             else:
                 gen = torch.Generator(device=self.dev)
                 gen.manual_seed(hash((self.seed, "param", pid)) & 0x7FFFFFFF)
-                fan_in = g[pid].dims[0]
-                full = torch.randn(g[pid].dims, generator=gen, device=self.dev) / math.sqrt(fan_in)
+                # GPT-style init (std 0.02) keeps the 24-block residual stream O(1)
+                full = torch.randn(g[pid].dims, generator=gen, device=self.dev) * self.init_std
                 loc = full[tuple(slice(lo, hi) for lo, hi in box)]
                 self.master[off:off + sz].copy_(loc.reshape(-1))
                 del full
@@ -332,10 +344,11 @@ class StageRunner:
         """Bring two (possibly head-split 4-D) operands to a common batch form."""
         if a.dim() == b.dim():
             return a, b
+        # splitting the batch dim is a view for any strides (no copy)
         if a.dim() == 4 and b.dim() == 3:
-            return a, self._contig(b).view(a.shape[0], a.shape[1], *b.shape[1:])
+            return a, b.unflatten(0, (a.shape[0], a.shape[1]))
         if a.dim() == 3 and b.dim() == 4:
-            return self._contig(a).view(b.shape[0], b.shape[1], *a.shape[1:]), b
+            return a.unflatten(0, (b.shape[0], b.shape[1])), b
         raise ExecError(f"gemm operand ranks {a.dim()} / {b.dim()}")
 
     def _run_matmul(self, mb: int, op: _Op) -> Optional[torch.Tensor]:
@@ -349,6 +362,17 @@ class StageRunner:
             self._gemm(a, b, out_view, beta=1.0)
             return None
         shape = tuple(a.shape[:-2]) + (a.shape[-2], b.shape[-1])
+        if op.extra is not None and not k_axes:
+            # the only consumer is a head merge: write straight into (T, h) layout
+            kind, (B, H, s, d) = op.extra
+            buf = torch.empty(B * s, H * d, dtype=torch.bfloat16, device=self.dev)
+            v4 = buf.view(B, s, H, d)
+            out = v4.permute(0, 2, 1, 3) if kind == "merge" else v4.permute(0, 2, 3, 1)
+            a4, b4 = a, b
+            if a4.dim() == 3:
+                a4, b4 = a4.unflatten(0, (B, H)), b4.unflatten(0, (B, H))
+            self._gemm(a4, b4, out)
+            return out
         out = torch.empty(shape, dtype=torch.bfloat16, device=self.dev)
         self._gemm(a, b, out)
         if k_axes:
