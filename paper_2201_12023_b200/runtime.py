@@ -36,6 +36,7 @@ from .layout import all_local, canonical, matmul_algo, relayout_moves, reshape_r
 from .plan import (ExecPlan, Mesh, PlanError, Spec, box_numel, device_box, load_plan,
                    local_dims, replicated)
 from .schedule import GPIPE, Instr, Program, build_program
+from .xmesh import recvs_of, sends_of
 
 
 class ExecError(RuntimeError):
@@ -527,18 +528,19 @@ class StageRunner:
         bd = ins.boundary
         mb = ins.microbatch
         vals = self.vals.setdefault(mb, {})
-        recvs = []
+        outs = []
         for bt in bd.tensors:
             node = self.graph[bt.node]
             dspec = canonical(bt.dst_spec, self.mesh)
-            mine = device_box(node.dims, dspec, self.mesh, self.me)
             out = torch.empty(local_dims(node.dims, dspec, self.mesh), dtype=torch.bfloat16,
                               device=self.dev)
             vals[bt.node] = out
-            for t in bt.xplan.transfers:
-                if t.dst_device == self.me:
-                    buf = torch.empty(box_numel(t.box), dtype=torch.bfloat16, device=self.dev)
-                    recvs.append((buf, t.src_device, out, _lo(_rel(t.box, _lo(mine))), _ext(t.box)))
+            outs.append((out, _lo(device_box(node.dims, dspec, self.mesh, self.me))))
+        recvs = []
+        for k, t in recvs_of(bd, self.me):
+            out, origin = outs[k]
+            buf = torch.empty(box_numel(t.box), dtype=torch.bfloat16, device=self.dev)
+            recvs.append((buf, t.src_device, out, _lo(_rel(t.box, origin)), _ext(t.box)))
         if recvs:
             works = self.comm.p2p([], [(b, s) for b, s, *_ in recvs],
                                   self.comm.boundary_group(bd, self.plan))
@@ -589,14 +591,12 @@ class StageRunner:
         bd = ins.boundary
         mb = ins.microbatch
         sends = []
-        for bt in bd.tensors:
+        for k, t in sends_of(bd, self.me):
+            bt = bd.tensors[k]
             node = self.graph[bt.node]
             v = self._as3(self.value(mb, bt.node))
             mine = _lo(device_box(node.dims, self.spec(bt.node), self.mesh, self.me))
-            for t in bt.xplan.transfers:
-                if t.src_device == self.me:
-                    sends.append((native.pack_box(v, _lo(_rel(t.box, mine)), _ext(t.box)),
-                                  t.dst_device))
+            sends.append((native.pack_box(v, _lo(_rel(t.box, mine)), _ext(t.box)), t.dst_device))
         if sends:
             self.pending_sends += self.comm.p2p(sends, [], self.comm.boundary_group(bd, self.plan))
 

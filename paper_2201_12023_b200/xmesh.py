@@ -163,3 +163,15 @@ def stage_boundaries(plan: ExecPlan, optimize: bool = True) -> list[Boundary]:
                 recv += node.nbytes // st.mesh.group_extent(dspec.axes_used())
             out.append(Boundary(p, st.index, tuple(tensors), recv))
     return out
+
+
+def sends_of(bd: Boundary, device: int) -> list[tuple[int, Transfer]]:
+    """(tensor index, transfer) pairs `device` sends for boundary `bd`, in the
+    order every rank derives (tensor order, then transfer order)."""
+    return [(k, t) for k, bt in enumerate(bd.tensors) for t in bt.xplan.transfers
+            if t.src_device == device]
+
+
+def recvs_of(bd: Boundary, device: int) -> list[tuple[int, Transfer]]:
+    return [(k, t) for k, bt in enumerate(bd.tensors) for t in bt.xplan.transfers
+            if t.dst_device == device]
