@@ -121,7 +121,10 @@ class StageRunner:
         self.bound = bind(plan.graph)
         self.seed = seed
         self.adam = adam or AdamConfig()
-        self.init_std = 0.02
+        # GPT-2-style residual scaling: the IR has no LayerNorm, so every branch
+        # weight gets std 0.02/sqrt(2*blocks) to keep the residual stream O(1)
+        blocks = max(1, sum(1 for b in self.bound.values() if b.op in ("gelu", "softmax")) // 2)
+        self.init_std = 0.02 / math.sqrt(2 * blocks)
         self.inputs_fn = inputs
         self.host_inputs = host_inputs
         self.dev = torch.device("cuda", torch.cuda.current_device())
