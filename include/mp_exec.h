@@ -96,6 +96,20 @@ int mp_softmax_bwd(const void* y, const void* dy, void* dx, const float* rowdot,
 int mp_softmax_rowdot(const void* y, const void* dy, float* rowdot, int64_t rows,
                       int64_t cols, int64_t ld, void* stream);
 
+/* ---- fused attention (cluster bmm -> softmax -> bmm, graph.py:297-302, and its
+ * structural backward graph.py:341-361), for stages whose softmax dim is local.
+ * Q/K/V/O/dO/dK/dV: (B*s, ld) bf16 row-major, head hh in columns [hh*d, hh*d+d);
+ * d must be 64, s a multiple of 128.  lse, dvec: fp32 [B*H, s].  dq_acc: fp32
+ * (B*s, ld), zeroed by the caller, accumulated atomically (cast afterwards).
+ * Non-causal softmax(scale * q k^T). */
+int mp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld, float scale,
+                void* stream);
+int mp_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                const void* dout, const float* lse, float* dvec, float* dq_acc,
+                void* dk, void* dv, int64_t B, int64_t H, int64_t s, int64_t d,
+                int64_t ld, float scale, void* stream);
+
 /* ---- box pack / unpack (cross-mesh Transfer, reshard.py:32-37,97-108) -----
  * Copies the sub-box [lo, lo+ext) of a strided tensor of rank <= 4 to / from
  * a dense buffer.  dims/strides in elements, elem_bytes in {2,4}. */

@@ -1,0 +1,655 @@
+// Fused attention for stages whose softmax dimension is local (SURVEY §2.1:
+// "when specs allow (softmax dim local), fuse scores -> softmax -> ctx into one
+// FMHA kernel").  It replaces the IR cluster
+//   scores = bmm(q_h, k_h^T) -> probs = softmax(scores / sqrt(d)) -> ctx = bmm(probs, v_h)
+// (reference graph.py:297-302) and its structural backward (graph.py:341-361)
+// without materialising scores / probs.
+//
+// Layout: Q, K, V, O, dO, dQ, dK, dV are (T, ld) row-major with head `hh` in
+// columns [hh*64, hh*64+64) and batch b in rows [b*s, b*s+s) — exactly the
+// (tokens, hidden) tensors of the projection matmuls, so head split / merge
+// stay views.  d = 64 (GPT-1.3B), s % 128 == 0.
+//
+// Forward (one CTA per 128-query tile of one (b, head)):
+//   warp 0     TMA: Q once, K/V tiles through a 2-stage ring
+//   warp 1     tcgen05.mma: S = Q K^T (TMEM, 128 cols), O += P V (TMEM, 64 cols)
+//   warps 2-5  softmax, one thread per query row: online max / sum in the log2
+//              domain with lazy O rescaling, P -> smem (128B-swizzled K-major),
+//              epilogue O / l -> bf16, LSE -> fp32
+// Backward (one CTA per 128-key tile, loop over query tiles, FA2 order):
+//   S^T = K Q^T, dP^T = V dO^T (TMEM); P^T = exp(S^T - LSE), dS^T = P^T (dP^T - D)
+//   (smem); dV += P^T dO, dK += dS^T Q (TMEM accumulators), dQ_i = dS K (TMEM) ->
+//   fp32 atomics.  The same swizzled smem tiles serve as K-major and MN-major
+//   operands, so no transposes are materialised.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include "common.cuh"
+#include "../../include/mp_exec.h"
+
+namespace mp {
+
+constexpr int FA_D = 64;
+constexpr int FA_BM = 128;   // query rows per tile
+constexpr int FA_BN = 128;   // keys per tile
+constexpr int FA_TILE = 128 * 64 * 2;  // 16 KB: 128 rows x 64 bf16, SW128
+
+// tcgen05.ld 32 lanes x 32b x 16 columns
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]));
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const void* tmap, uint64_t* bar, void* dst, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Store 8 bf16 (one 16-byte unit) of row r, unit u of a 128B-swizzled chunk.
+__device__ __forceinline__ void st_sw128(uint8_t* chunk, int r, int u, uint4 v) {
+  *reinterpret_cast<uint4*>(chunk + r * 128 + ((u ^ (r & 7)) << 4)) = v;
+}
+
+struct FaFwdParams {
+  int B, H, s, ld;
+  float scale_log2;  // log2(e) / sqrt(d)
+  uint16_t* O;
+  float* lse;        // [B*H, s]
+};
+
+// smem: Q 16K | K[2] 32K | V[2] 32K | P 32K | barriers
+constexpr int FA_FWD_SMEM = FA_TILE * 7 + 1024 + 256;
+
+__global__ void __launch_bounds__(192, 1)
+    fa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const FaFwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + FA_TILE;          // 2 stages
+  uint8_t* sV = smem + 3 * FA_TILE;      // 2 stages
+  uint8_t* sP = smem + 5 * FA_TILE;      // 2 chunks of 64 keys
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 7 * FA_TILE);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* s_free = bars + 6;
+  uint64_t* p_full = bars + 7;
+  uint64_t* o_done = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x;                  // query tile
+  const int bh = blockIdx.y;
+  const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
+  const int n_kv = p.s / FA_BN;
+  const int row0 = b * p.s;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 4);
+    mbar_init(p_full, 4);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tO = tmem + 128;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, FA_TILE);
+      tma_load_2d(&tmQ, q_full, sQ, hh * FA_D, row0 + qt * FA_BM);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * FA_TILE);
+        tma_load_2d(&tmK, &kv_full[st], sK + st * FA_TILE, hh * FA_D, row0 + j * FA_BN);
+        tma_load_2d(&tmV, &kv_full[st], sV + st * FA_TILE, hh * FA_D, row0 + j * FA_BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = umma_idesc_bf16(128, 128, 0, 0);   // Q K-major, K K-major
+      const uint32_t id_o = umma_idesc_bf16(128, 64, 0, 1);    // P K-major, V MN-major
+      mbar_wait(q_full, 0);
+      const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        if (j > 0) mbar_wait(s_free, (j - 1) & 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sK + st * FA_TILE);
+#pragma unroll
+        for (int kk = 0; kk < FA_D / 16; ++kk)
+          tc_mma_f16(tS, umma_desc_sw128(q_base + kk * 32, 16, 1024),
+                     umma_desc_sw128(k_base + kk * 32, 16, 1024), id_s, kk > 0);
+        tc_commit(s_full);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_s(j + 1);
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(sV + (j & 1) * FA_TILE);
+#pragma unroll
+        for (int kk = 0; kk < FA_BN / 16; ++kk) {
+          const uint64_t ad = umma_desc_sw128(p_base + (kk >> 2) * FA_TILE + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, 8192, 1024);
+          tc_mma_f16(tO, ad, bd, id_o, (j | kk) != 0);
+        }
+        tc_commit(&kv_empty[j & 1]);
+        tc_commit(o_done);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;                       // query row within the tile
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    float m_used = -INFINITY;                          // log2-domain running max
+    float l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t t16[16];
+        tmem_ld16(tS + lane_off + c * 16, t16);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) sr[c * 16 + e] = t16[e];
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sr[e]));
+      mx *= p.scale_log2;
+      // lazy rescale: only when the max grows by more than 2^8
+      const bool need = (mx > m_used + 8.f);
+      float alpha = 1.f;
+      if (need) {
+        alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
+        m_used = mx;
+      }
+      float sum = 0.f;
+      // P must not overwrite smem before PV_{j-1} has consumed it
+      if (j > 0) {
+        mbar_wait(o_done, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o16[16];
+            tmem_ld16(tO + lane_off + c * 16, o16);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o16[e] = __float_as_uint(__uint_as_float(o16[e]) * alpha);
+            tmem_st16(tO + lane_off + c * 16, o16);
+          }
+          tmem_st_wait();
+        }
+      }
+      l *= alpha;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float pv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            pv[e] = ex2(__uint_as_float(sr[ch * 64 + u * 8 + e]) * p.scale_log2 - m_used);
+            sum += pv[e];
+          }
+          st_sw128(sP + ch * FA_TILE, r, u,
+                   make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]),
+                              pack_bf2(pv[4], pv[5]), pack_bf2(pv[6], pv[7])));
+        }
+      }
+      l += sum;
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // epilogue
+    mbar_wait(o_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    const int grow = row0 + qt * FA_BM + r;
+    uint16_t* orow = p.O + (int64_t)grow * p.ld + hh * FA_D;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o16[16];
+      tmem_ld16(tO + lane_off + c * 16, o16);
+      tmem_ld_wait();
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+      dst[0] = make_uint4(pack_bf2(__uint_as_float(o16[0]) * inv, __uint_as_float(o16[1]) * inv),
+                          pack_bf2(__uint_as_float(o16[2]) * inv, __uint_as_float(o16[3]) * inv),
+                          pack_bf2(__uint_as_float(o16[4]) * inv, __uint_as_float(o16[5]) * inv),
+                          pack_bf2(__uint_as_float(o16[6]) * inv, __uint_as_float(o16[7]) * inv));
+      dst[1] = make_uint4(pack_bf2(__uint_as_float(o16[8]) * inv, __uint_as_float(o16[9]) * inv),
+                          pack_bf2(__uint_as_float(o16[10]) * inv, __uint_as_float(o16[11]) * inv),
+                          pack_bf2(__uint_as_float(o16[12]) * inv, __uint_as_float(o16[13]) * inv),
+                          pack_bf2(__uint_as_float(o16[14]) * inv, __uint_as_float(o16[15]) * inv));
+    }
+    // natural-log LSE of the scaled scores: ln(l) + m_used * ln 2
+    p.lse[(int64_t)bh * p.s + qt * FA_BM + r] = logf(l) + m_used * 0.6931471805599453f;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------ backward
+struct FaBwdParams {
+  int B, H, s, ld;
+  float scale;        // 1/sqrt(d)
+  const float* lse;   // [B*H, s]
+  const float* dvec;  // D = rowsum(dO * O), [B*H, s]
+  float* dQacc;       // fp32 (T, ld), zero-initialised
+  uint16_t* dK;
+  uint16_t* dV;
+};
+
+// smem: K 16K | V 16K | Q[2] 32K | dO[2] 32K | P^T 32K | dS^T 32K | lse/D 2x2x512 | barriers
+constexpr int FA_BWD_SMEM = FA_TILE * 10 + 4096 + 1024 + 256;
+
+__global__ void __launch_bounds__(192, 1)
+    fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                  const FaBwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + FA_TILE;
+  uint8_t* sQ = smem + 2 * FA_TILE;    // [2]
+  uint8_t* sdO = smem + 4 * FA_TILE;   // [2]
+  uint8_t* sPt = smem + 6 * FA_TILE;   // 2 chunks (queries 0-63 | 64-127)
+  uint8_t* sdSt = smem + 8 * FA_TILE;  // 2 chunks
+  float* sLse = reinterpret_cast<float*>(smem + 10 * FA_TILE);   // [2][128]
+  float* sD = sLse + 256;                                        // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 10 * FA_TILE + 4096);
+  uint64_t* kv_full = bars;         // K, V
+  uint64_t* q_full = bars + 1;      // [2] Q_i, dO_i (+ lse/D via the producer warp)
+  uint64_t* q_empty = bars + 3;     // [2]
+  uint64_t* st_full = bars + 5;     // S^T and dP^T in TMEM
+  uint64_t* ps_full = bars + 6;     // P^T / dS^T in smem (4 warps)
+  uint64_t* mma_done = bars + 7;    // dV/dK/dQ MMAs of tile i finished (smem free)
+  uint64_t* dq_full = bars + 8;
+  uint64_t* dq_free = bars + 9;     // 4 warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kt = blockIdx.x;      // key tile
+  const int bh = blockIdx.y;
+  const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
+  const int n_q = p.s / FA_BM;
+  const int row0 = b * p.s;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmdO);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1 + 32);   // tx arrive + 32 lanes copying lse / D
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(st_full, 1);
+    mbar_init(ps_full, 4);
+    mbar_init(mma_done, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tSt = tmem, tdPt = tmem + 128, tdV = tmem + 256, tdK = tmem + 320,
+                 tdQ = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * FA_TILE);
+      tma_load_2d(&tmK, kv_full, sK, hh * FA_D, row0 + kt * FA_BN);
+      tma_load_2d(&tmV, kv_full, sV, hh * FA_D, row0 + kt * FA_BN);
+    }
+    for (int i = 0; i < n_q; ++i) {
+      const int st = i & 1;
+      mbar_wait(&q_empty[st], ((i >> 1) & 1) ^ 1);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&q_full[st], 2 * FA_TILE);
+        tma_load_2d(&tmQ, &q_full[st], sQ + st * FA_TILE, hh * FA_D, row0 + i * FA_BM);
+        tma_load_2d(&tmdO, &q_full[st], sdO + st * FA_TILE, hh * FA_D, row0 + i * FA_BM);
+      }
+      const int64_t base = (int64_t)bh * p.s + i * FA_BM;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        sLse[st * 128 + k * 32 + lane] = p.lse[base + k * 32 + lane];
+        sD[st * 128 + k * 32 + lane] = p.dvec[base + k * 32 + lane];
+      }
+      mbar_arrive(&q_full[st]);   // release semantics publish the lse / D stores
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_st = umma_idesc_bf16(128, 128, 0, 0);  // K/V (K-major) x Q/dO (K-major)
+      const uint32_t id_acc = umma_idesc_bf16(128, 64, 0, 1);  // P^T/dS^T (K-major) x dO/Q (MN)
+      const uint32_t id_dq = umma_idesc_bf16(128, 64, 1, 1);   // dS (MN-major) x K (MN-major)
+      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
+      const uint32_t pt_base = smem_u32(sPt), dst_base = smem_u32(sdSt);
+      mbar_wait(kv_full, 0);
+      for (int i = 0; i < n_q; ++i) {
+        const int st = i & 1;
+        mbar_wait(&q_full[st], (i >> 1) & 1);
+        if (i > 0) mbar_wait(ps_full, (i - 1) & 1);   // S^T / dP^T TMEM consumed
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ + st * FA_TILE);
+        const uint32_t do_base = smem_u32(sdO + st * FA_TILE);
+#pragma unroll
+        for (int kk = 0; kk < FA_D / 16; ++kk) {
+          tc_mma_f16(tSt, umma_desc_sw128(k_base + kk * 32, 16, 1024),
+                     umma_desc_sw128(q_base + kk * 32, 16, 1024), id_st, kk > 0);
+          tc_mma_f16(tdPt, umma_desc_sw128(v_base + kk * 32, 16, 1024),
+                     umma_desc_sw128(do_base + kk * 32, 16, 1024), id_st, kk > 0);
+        }
+        tc_commit(st_full);
+        mbar_wait(ps_full, i & 1);
+        tc_fence_after();
+        // dV += P^T dO ; dK += dS^T Q   (K = 128 queries: 2 chunks x 4 steps)
+#pragma unroll
+        for (int kk = 0; kk < FA_BM / 16; ++kk) {
+          const uint32_t aoff = (kk >> 2) * FA_TILE + (kk & 3) * 32;
+          tc_mma_f16(tdV, umma_desc_sw128(pt_base + aoff, 16, 1024),
+                     umma_desc_sw128(do_base + kk * 2048, 8192, 1024), id_acc, (i | kk) != 0);
+          tc_mma_f16(tdK, umma_desc_sw128(dst_base + aoff, 16, 1024),
+                     umma_desc_sw128(q_base + kk * 2048, 8192, 1024), id_acc, (i | kk) != 0);
+        }
+        // dQ_i = dS K   (M = 128 queries from dS^T as MN-major A, K = 128 keys)
+        if (i > 0) mbar_wait(dq_free, (i - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < FA_BN / 16; ++kk)
+          tc_mma_f16(tdQ, umma_desc_sw128(dst_base + kk * 2048, FA_TILE, 1024),
+                     umma_desc_sw128(k_base + kk * 2048, 8192, 1024), id_dq, kk > 0);
+        tc_commit(dq_full);
+        tc_commit(mma_done);
+        tc_commit(&q_empty[st]);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;                        // key row (S^T / dP^T lane)
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const float sl2 = p.scale * 1.4426950408889634f;
+    for (int i = 0; i < n_q; ++i) {
+      const int st = i & 1;
+      mbar_wait(st_full, i & 1);
+      tc_fence_after();
+      // P^T / dS^T smem is free once the MMAs of tile i-1 completed
+      if (i > 0) mbar_wait(mma_done, (i - 1) & 1);
+      const float* lse = sLse + st * 128;
+      const float* dv = sD + st * 128;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {          // 16 queries per chunk
+        uint32_t s16[16], d16[16];
+        tmem_ld16(tSt + lane_off + c * 16, s16);
+        tmem_ld16(tdPt + lane_off + c * 16, d16);
+        tmem_ld_wait();
+        float pv[16], ds[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int qq = c * 16 + e;
+          pv[e] = ex2(__uint_as_float(s16[e]) * sl2 - lse[qq] * 1.4426950408889634f);
+          ds[e] = pv[e] * (__uint_as_float(d16[e]) - dv[qq]) * p.scale;
+        }
+        const int ch = c >> 2, u0 = (c & 3) * 2;
+        st_sw128(sPt + ch * FA_TILE, r, u0,
+                 make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]), pack_bf2(pv[4], pv[5]),
+                            pack_bf2(pv[6], pv[7])));
+        st_sw128(sPt + ch * FA_TILE, r, u0 + 1,
+                 make_uint4(pack_bf2(pv[8], pv[9]), pack_bf2(pv[10], pv[11]),
+                            pack_bf2(pv[12], pv[13]), pack_bf2(pv[14], pv[15])));
+        st_sw128(sdSt + ch * FA_TILE, r, u0,
+                 make_uint4(pack_bf2(ds[0], ds[1]), pack_bf2(ds[2], ds[3]), pack_bf2(ds[4], ds[5]),
+                            pack_bf2(ds[6], ds[7])));
+        st_sw128(sdSt + ch * FA_TILE, r, u0 + 1,
+                 make_uint4(pack_bf2(ds[8], ds[9]), pack_bf2(ds[10], ds[11]),
+                            pack_bf2(ds[12], ds[13]), pack_bf2(ds[14], ds[15])));
+      }
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ps_full);
+      // dQ_i: this thread owns query row r of tile i
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      float* dq = p.dQacc + (int64_t)(row0 + i * FA_BM + r) * p.ld + hh * FA_D;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t t16[16];
+        tmem_ld16(tdQ + lane_off + c * 16, t16);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 16; e += 4)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 16 + e),
+                       "f"(__uint_as_float(t16[e])), "f"(__uint_as_float(t16[e + 1])),
+                       "f"(__uint_as_float(t16[e + 2])), "f"(__uint_as_float(t16[e + 3]))
+                       : "memory");
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_free);
+    }
+    // dK, dV epilogue: key row r
+    mbar_wait(mma_done, (n_q - 1) & 1);
+    tc_fence_after();
+    const int64_t grow = row0 + kt * FA_BN + r;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t tacc = which ? tdV : tdK;
+      uint16_t* out = (which ? p.dV : p.dK) + grow * p.ld + hh * FA_D;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t t16[16];
+        tmem_ld16(tacc + lane_off + c * 16, t16);
+        tmem_ld_wait();
+        uint4* dst = reinterpret_cast<uint4*>(out + c * 16);
+        dst[0] = make_uint4(pack_bf2(__uint_as_float(t16[0]), __uint_as_float(t16[1])),
+                            pack_bf2(__uint_as_float(t16[2]), __uint_as_float(t16[3])),
+                            pack_bf2(__uint_as_float(t16[4]), __uint_as_float(t16[5])),
+                            pack_bf2(__uint_as_float(t16[6]), __uint_as_float(t16[7])));
+        dst[1] = make_uint4(pack_bf2(__uint_as_float(t16[8]), __uint_as_float(t16[9])),
+                            pack_bf2(__uint_as_float(t16[10]), __uint_as_float(t16[11])),
+                            pack_bf2(__uint_as_float(t16[12]), __uint_as_float(t16[13])),
+                            pack_bf2(__uint_as_float(t16[14]), __uint_as_float(t16[15])));
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// D[bh, t] = sum_d dO * O   (warp per row of 64), and dQacc zeroing is done by the caller
+__global__ void fa_bwd_pre_kernel(const uint16_t* __restrict__ O, const uint16_t* __restrict__ dO,
+                                  float* __restrict__ dvec, int B, int H, int s, int ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)B * H * s;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t w = blockIdx.x * wpb + (threadIdx.x >> 5); w < rows; w += (int64_t)gridDim.x * wpb) {
+    const int64_t bh = w / s, t = w - (w / s) * s;
+    const int64_t b = bh / H, hh = bh - (bh / H) * H;
+    const int64_t off = (b * s + t) * ld + hh * FA_D + lane * 2;
+    uint32_t o = *reinterpret_cast<const uint32_t*>(O + off);
+    uint32_t g = *reinterpret_cast<const uint32_t*>(dO + off);
+    float acc = bf2f(o & 0xffff) * bf2f(g & 0xffff) + bf2f(o >> 16) * bf2f(g >> 16);
+#pragma unroll
+    for (int k = 16; k; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
+    if (lane == 0) dvec[w] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ host
+static PFN_cuTensorMapEncodeTiled_v12000 fa_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// (rows x ld) bf16 matrix, box 64 cols x 128 rows, 128B swizzle
+static int fa_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ld) {
+  auto enc = fa_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 1;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return 1;
+  }
+  return 0;
+}
+
+static bool fa_args_ok(const void* p, int64_t ld) {
+  return p && (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 8 == 0);
+}
+
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" int mp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                           int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld, float scale,
+                           void* stream) {
+  clear_error();
+  MP_CHECK_ARG(d == FA_D, "head dim must be 64");
+  MP_CHECK_ARG(s % 128 == 0 && s > 0, "sequence length must be a multiple of 128");
+  MP_CHECK_ARG(ld >= H * d, "row stride smaller than heads*d");
+  MP_CHECK_ARG(fa_args_ok(q, ld) && fa_args_ok(k, ld) && fa_args_ok(v, ld) && fa_args_ok(o, ld) &&
+                   lse,
+               "pointers must be 16-byte aligned with 8-element aligned rows");
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = fa_map(&mq, q, B * s, ld)) || (rc = fa_map(&mk, k, B * s, ld)) ||
+      (rc = fa_map(&mv, v, B * s, ld)))
+    return rc;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(fa_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_FWD_SMEM);
+    configured = true;
+  }
+  FaFwdParams p{(int)B, (int)H, (int)s, (int)ld, scale * 1.4426950408889634f,
+                reinterpret_cast<uint16_t*>(o), lse};
+  dim3 grid((unsigned)(s / FA_BM), (unsigned)(B * H));
+  fa_fwd_kernel<<<grid, 192, FA_FWD_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, p);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int mp_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                           const void* dout, const float* lse, float* dvec, float* dq_acc,
+                           void* dk, void* dv, int64_t B, int64_t H, int64_t s, int64_t d,
+                           int64_t ld, float scale, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(d == FA_D, "head dim must be 64");
+  MP_CHECK_ARG(s % 128 == 0 && s > 0, "sequence length must be a multiple of 128");
+  MP_CHECK_ARG(fa_args_ok(q, ld) && fa_args_ok(k, ld) && fa_args_ok(v, ld) && fa_args_ok(o, ld) &&
+                   fa_args_ok(dout, ld) && fa_args_ok(dk, ld) && fa_args_ok(dv, ld) && lse &&
+                   dvec && dq_acc,
+               "bad pointers");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  {
+    const int64_t rows = B * H * s;
+    int64_t blocks = (rows * 32 + 255) / 256;
+    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+    fa_bwd_pre_kernel<<<(unsigned)blocks, 256, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(o), reinterpret_cast<const uint16_t*>(dout), dvec,
+        (int)B, (int)H, (int)s, (int)ld);
+    MP_CHECK_LAUNCH();
+  }
+  CUtensorMap mq, mk, mv, mdo;
+  int rc;
+  if ((rc = fa_map(&mq, q, B * s, ld)) || (rc = fa_map(&mk, k, B * s, ld)) ||
+      (rc = fa_map(&mv, v, B * s, ld)) || (rc = fa_map(&mdo, dout, B * s, ld)))
+    return rc;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_BWD_SMEM);
+    configured = true;
+  }
+  FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, scale, lse, dvec, dq_acc,
+                reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
+  dim3 grid((unsigned)(s / FA_BN), (unsigned)(B * H));
+  fa_bwd_kernel<<<grid, 192, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, p);
+  MP_CHECK_LAUNCH();
+  return 0;
+}

@@ -39,6 +39,10 @@ EXPORTS = {
     "mp_softmax_apply": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
     "mp_softmax_bwd": ([c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
     "mp_softmax_rowdot": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp], c_int),
+    "mp_attn_fwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_f32,
+                     c_vp], c_int),
+    "mp_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
+                     c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
     "mp_pack_box": ([c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp, c_vp], c_int),
     "mp_unpack_box": ([c_vp, c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp], c_int),
     "mp_adam_step": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_f32, c_f32, c_f32, c_f32, c_f32,
@@ -279,6 +283,40 @@ def softmax_bwd(y: torch.Tensor, dy: torch.Tensor, s: float, rowdot: Optional[to
                                  rowdot.data_ptr() if rowdot is not None else None, rows, cols, ld,
                                  float(s), _stream(stream)), "mp_softmax_bwd")
     return out
+
+
+# --------------------------------------------------------------------------- attention
+
+def _heads_view(t: torch.Tensor, name: str):
+    """(T, ld) bf16 with unit column stride -> (ptr, ld)."""
+    _require(t, torch.bfloat16, name)
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise NativeError(f"{name} must be a (tokens, hidden) row-major view")
+    return t.data_ptr(), t.stride(0)
+
+
+def attn_fwd(q, k, v, o, lse, B: int, H: int, s: int, d: int, scale: float, stream=None):
+    """Fused non-causal attention forward on (B*s, H*d) tensors; lse fp32 [B*H, s]."""
+    ptrs = [_heads_view(t, n) for t, n in ((q, "q"), (k, "k"), (v, "v"), (o, "o"))]
+    lds = {ld for _, ld in ptrs}
+    if len(lds) != 1:
+        raise NativeError("q/k/v/o must share the row stride")
+    _require(lse, torch.float32, "lse")
+    _check(load().mp_attn_fwd(ptrs[0][0], ptrs[1][0], ptrs[2][0], ptrs[3][0], lse.data_ptr(),
+                              B, H, s, d, lds.pop(), float(scale), _stream(stream)), "mp_attn_fwd")
+
+
+def attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, B: int, H: int, s: int, d: int,
+             scale: float, stream=None):
+    ptrs = [_heads_view(t, n) for t, n in ((q, "q"), (k, "k"), (v, "v"), (o, "o"), (dout, "dout"),
+                                            (dk, "dk"), (dv, "dv"))]
+    lds = {ld for _, ld in ptrs} | {dq_acc.stride(0)}
+    if len(lds) != 1:
+        raise NativeError("attention operands must share the row stride")
+    _check(load().mp_attn_bwd(ptrs[0][0], ptrs[1][0], ptrs[2][0], ptrs[3][0], ptrs[4][0],
+                              lse.data_ptr(), dvec.data_ptr(), dq_acc.data_ptr(), ptrs[5][0],
+                              ptrs[6][0], B, H, s, d, lds.pop(), float(scale), _stream(stream)),
+           "mp_attn_bwd")
 
 
 # --------------------------------------------------------------------------- boxes

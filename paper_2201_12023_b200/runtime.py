@@ -135,6 +135,7 @@ class StageRunner:
         self.step_count = 0
         self.vals: dict[int, dict[int, torch.Tensor]] = {}
         self.cache: dict[int, dict] = {}
+        self.aux: dict[int, dict] = {}
         self.loss_acc = torch.zeros(1, dtype=torch.float32, device=self.dev)
         self.outputs: dict[int, torch.Tensor] = {}
         self.keep_outputs = False
@@ -204,6 +205,139 @@ class StageRunner:
         # fwd output of the graph (for the loss seed / checks)
         self.seed_ids = [o.nid for o in self.bwd_ops if o.op == "seed"]
         self.members = members
+        self.fuse_attention = os.environ.get("MPEXEC_FUSE_ATTENTION", "1") != "0"
+        self.attn_clusters = self._fuse_attention() if self.fuse_attention else []
+
+    # ------------------------------------------------------------------ fusion
+    def _fuse_attention(self) -> list[dict]:
+        """Replace each eligible attention cluster (graph.py:297-302 and its
+        backward, graph.py:341-361) by the fused tcgen05 kernels.  Eligible when
+        every node of the cluster is local to the device (stage of one device or
+        all-replicated specs: the softmax dim is then local) and d = 64,
+        s % 128 == 0.  Returns the clusters fused."""
+        g = self.graph
+        b = self.bound
+        cons = self.cons
+        colo: dict[int, list[int]] = {}
+        for nid in self.st.op_ids:
+            c = g[nid].colocate_with
+            if c is not None:
+                colo.setdefault(c, []).append(nid)
+        clusters = []
+        for op in list(self.fwd_ops):
+            S = op.nid
+            if op.op != "bmm":
+                continue
+            qh, kh = g[S].inputs
+            if b[qh].op != "split" or b[kh].op != "split_t":
+                continue
+            fwd_users = [c for c, _ in cons[S] if g[c].colocate_with is None]
+            if len(fwd_users) != 1 or b[fwd_users[0]].op != "softmax":
+                continue
+            P = fwd_users[0]
+            p_fwd = [c for c, _ in cons[P] if g[c].colocate_with is None]
+            if len(p_fwd) != 1 or b[p_fwd[0]].op != "bmm" or g[p_fwd[0]].inputs[0] != P:
+                continue
+            C = p_fwd[0]
+            vh = g[C].inputs[1]
+            if b[vh].op != "split":
+                continue
+            Bn, H, sq, d = b[qh].heads
+            if d != 64 or sq % 128 or b[kh].heads != (Bn, H, sq, d) or b[vh].heads != (Bn, H, sq, d):
+                continue
+            bwd = sorted(colo.get(C, []) + colo.get(P, []) + colo.get(S, []))
+            byk = {}
+            for nid in bwd:
+                byk.setdefault(b[nid].op, []).append(nid)
+            try:
+                dprobs = [n for n in colo.get(C, []) if b[n].op == "bmm" and g[n].inputs[0] != P
+                          and b[g[n].inputs[1]].op == "transpose"][0]
+                dvh = [n for n in colo.get(C, []) if b[n].op == "bmm" and n != dprobs][0]
+                dS = [n for n in colo.get(P, []) if b[n].op == "softmax_bwd"][0]
+                dqh = [n for n in colo.get(S, []) if b[n].op == "bmm" and g[n].inputs[0] == dS][0]
+                dkh = [n for n in colo.get(S, []) if b[n].op == "bmm" and n != dqh][0]
+            except IndexError:
+                continue
+            gC = g[dvh].inputs[1]                  # dL/dctx (a head split of dL/dctx2)
+            if b[gC].op != "split" or g[dprobs].inputs[0] != gC:
+                continue
+            nodes = [S, P, C, qh, kh, vh, gC] + bwd
+            local = self.mesh.size == 1 or all(self.spec(n).is_replicated() for n in nodes)
+            if not local or any(n in self.st.output_specs for n in [S, P, C] + bwd):
+                continue
+            # every cluster output consumed only inside the cluster or by one merge
+            outs_ok = True
+            for n, want in ((C, "merge"), (dqh, "merge"), (dkh, "merge_t"), (dvh, "merge")):
+                users = [c for c, _ in cons[n] if c not in bwd]
+                if len(users) != 1 or b[users[0]].op != want:
+                    outs_ok = False
+            if not outs_ok:
+                continue
+            cl = dict(S=S, P=P, C=C, qh=qh, kh=kh, vh=vh, gC=gC, dqh=dqh, dkh=dkh, dvh=dvh,
+                      q=g[qh].inputs[0], k=g[kh].inputs[0], v=g[vh].inputs[0],
+                      dctx2=g[gC].inputs[0], heads=(Bn, H, sq, d),
+                      scale=b[P].softmax_scale, bwd=set(bwd))
+            clusters.append(cl)
+        for cl in clusters:
+            fwd_ops = []
+            for o in self.fwd_ops:
+                if o.nid == cl["S"]:
+                    fo = _Op(cl["C"], "attn_fwd", self.bound[cl["C"]], [], self.spec(cl["C"]))
+                    fo.extra = cl
+                    fwd_ops.append(fo)
+                elif o.nid in (cl["P"], cl["C"]):
+                    continue
+                else:
+                    fwd_ops.append(o)
+            self.fwd_ops = fwd_ops
+            bwd_ops = []
+            placed = False
+            for o in self.bwd_ops:
+                if o.nid in cl["bwd"]:
+                    if not placed:
+                        bo = _Op(cl["dqh"], "attn_bwd", self.bound[cl["dqh"]], [], self.spec(cl["dqh"]))
+                        bo.extra = cl
+                        bwd_ops.append(bo)
+                        placed = True
+                    continue
+                bwd_ops.append(o)
+            self.bwd_ops = bwd_ops
+        return clusters
+
+    def _run_attn_fwd(self, mb: int, op: _Op):
+        cl = op.extra
+        Bn, H, s, d = cl["heads"]
+        rep = replicated(2)
+        q = self._contig(self.get(mb, cl["q"], rep))
+        k = self._contig(self.get(mb, cl["k"], rep))
+        v = self._contig(self.get(mb, cl["v"], rep))
+        o = torch.empty(Bn * s, H * d, dtype=torch.bfloat16, device=self.dev)
+        lse = torch.empty(Bn * H, s, dtype=torch.float32, device=self.dev)
+        native.attn_fwd(q, k, v, o, lse, Bn, H, s, d, cl["scale"])
+        self.aux.setdefault(mb, {})[cl["S"]] = (o, lse)
+        return o.view(Bn, s, H, d).permute(0, 2, 1, 3)       # logical ctx (B*H, s, d)
+
+    def _run_attn_bwd(self, mb: int, op: _Op):
+        cl = op.extra
+        Bn, H, s, d = cl["heads"]
+        rep = replicated(2)
+        q = self._contig(self.get(mb, cl["q"], rep))
+        k = self._contig(self.get(mb, cl["k"], rep))
+        v = self._contig(self.get(mb, cl["v"], rep))
+        dout = self._contig(self.get(mb, cl["dctx2"], rep))
+        o, lse = self.aux[mb][cl["S"]]
+        T, hdim = Bn * s, H * d
+        dvec = torch.empty(Bn * H, s, dtype=torch.float32, device=self.dev)
+        dq_acc = torch.zeros(T, hdim, dtype=torch.float32, device=self.dev)
+        dk = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
+        dv = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
+        native.attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, Bn, H, s, d, cl["scale"])
+        dq = native.cast_f32_bf16(dq_acc, torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev))
+        vals = self.vals[mb]
+        vals[cl["dqh"]] = dq.view(Bn, s, H, d).permute(0, 2, 1, 3)
+        vals[cl["dkh"]] = dk.view(Bn, s, H, d).permute(0, 2, 3, 1)
+        vals[cl["dvh"]] = dv.view(Bn, s, H, d).permute(0, 2, 1, 3)
+        return None
 
     # ------------------------------------------------------------------ params
     def _init_params(self, init: Optional[dict[int, np.ndarray]]):
@@ -515,6 +649,10 @@ class StageRunner:
             try:
                 if op.op == "input":
                     out = self._load_input(mb, op)
+                elif op.op == "attn_fwd":
+                    out = self._run_attn_fwd(mb, op)
+                elif op.op == "attn_bwd":
+                    out = self._run_attn_bwd(mb, op)
                 elif op.op in ("matmul", "bmm"):
                     out = self._run_matmul(mb, op)
                 elif self.graph[op.nid].kind == "reshape":
@@ -607,6 +745,7 @@ class StageRunner:
         if ins.buffer and ins.buffer.startswith("act"):
             self.vals.pop(ins.microbatch, None)
             self.cache.pop(ins.microbatch, None)
+            self.aux.pop(ins.microbatch, None)
 
     # ------------------------------------------------------------------ optimizer
     def reduce_grads(self):
