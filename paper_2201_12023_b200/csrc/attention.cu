@@ -83,10 +83,15 @@ struct FaFwdParams {
   float* lse;        // [B*H, s]
 };
 
-// smem: Q 16K | K[2] 32K | V[2] 32K | P 32K | barriers
-constexpr int FA_FWD_SMEM = FA_TILE * 7 + 1024 + 256;
+// smem: Q 16K | K[2] 32K | V 16K | P 32K | barriers  (97 KB: two CTAs per SM)
+constexpr int FA_FWD_SMEM = FA_TILE * 6 + 1024 + 256;
 
-__global__ void __launch_bounds__(192, 1)
+// tcgen05.ld 32 lanes x 32b x 32 columns
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  tmem_ld_32x32b_x32(taddr, r);
+}
+
+__global__ void __launch_bounds__(192, 2)
     fa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const FaFwdParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -94,17 +99,19 @@ __global__ void __launch_bounds__(192, 1)
                                              ~(uintptr_t)1023);
   uint8_t* sQ = smem;
   uint8_t* sK = smem + FA_TILE;          // 2 stages
-  uint8_t* sV = smem + 3 * FA_TILE;      // 2 stages
-  uint8_t* sP = smem + 5 * FA_TILE;      // 2 chunks of 64 keys
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 7 * FA_TILE);
+  uint8_t* sV = smem + 3 * FA_TILE;      // 1 stage
+  uint8_t* sP = smem + 4 * FA_TILE;      // 2 chunks of 64 keys
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * FA_TILE);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* s_free = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_done = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* k_empty = bars + 3;   // [2]
+  uint64_t* v_full = bars + 5;
+  uint64_t* v_empty = bars + 6;
+  uint64_t* s_full = bars + 7;
+  uint64_t* s_free = bars + 8;
+  uint64_t* p_full = bars + 9;
+  uint64_t* o_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x;                  // query tile
@@ -119,9 +126,11 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tmV);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
     }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
     mbar_init(s_full, 1);
     mbar_init(s_free, 4);
     mbar_init(p_full, 4);
@@ -141,10 +150,12 @@ __global__ void __launch_bounds__(192, 1)
       tma_load_2d(&tmQ, q_full, sQ, hh * FA_D, row0 + qt * FA_BM);
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], 2 * FA_TILE);
-        tma_load_2d(&tmK, &kv_full[st], sK + st * FA_TILE, hh * FA_D, row0 + j * FA_BN);
-        tma_load_2d(&tmV, &kv_full[st], sV + st * FA_TILE, hh * FA_D, row0 + j * FA_BN);
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], FA_TILE);
+        tma_load_2d(&tmK, &k_full[st], sK + st * FA_TILE, hh * FA_D, row0 + j * FA_BN);
+        mbar_wait(v_empty, (j & 1) ^ 1);
+        mbar_arrive_expect_tx(v_full, FA_TILE);
+        tma_load_2d(&tmV, v_full, sV, hh * FA_D, row0 + j * FA_BN);
       }
     }
   } else if (warp == 1) {
@@ -152,10 +163,10 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t id_s = umma_idesc_bf16(128, 128, 0, 0);   // Q K-major, K K-major
       const uint32_t id_o = umma_idesc_bf16(128, 64, 0, 1);    // P K-major, V MN-major
       mbar_wait(q_full, 0);
-      const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
+      const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP), v_base = smem_u32(sV);
       auto issue_s = [&](int j) {
         const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&k_full[st], (j >> 1) & 1);
         if (j > 0) mbar_wait(s_free, (j - 1) & 1);
         tc_fence_after();
         const uint32_t k_base = smem_u32(sK + st * FA_TILE);
@@ -164,20 +175,21 @@ __global__ void __launch_bounds__(192, 1)
           tc_mma_f16(tS, umma_desc_sw128(q_base + kk * 32, 16, 1024),
                      umma_desc_sw128(k_base + kk * 32, 16, 1024), id_s, kk > 0);
         tc_commit(s_full);
+        tc_commit(&k_empty[st]);
       };
       issue_s(0);
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) issue_s(j + 1);
         mbar_wait(p_full, j & 1);
+        mbar_wait(v_full, j & 1);
         tc_fence_after();
-        const uint32_t v_base = smem_u32(sV + (j & 1) * FA_TILE);
 #pragma unroll
         for (int kk = 0; kk < FA_BN / 16; ++kk) {
           const uint64_t ad = umma_desc_sw128(p_base + (kk >> 2) * FA_TILE + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, 8192, 1024);
           tc_mma_f16(tO, ad, bd, id_o, (j | kk) != 0);
         }
-        tc_commit(&kv_empty[j & 1]);
+        tc_commit(v_empty);
         tc_commit(o_done);
       }
     }
@@ -190,21 +202,16 @@ __global__ void __launch_bounds__(192, 1)
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(s_full, j & 1);
       tc_fence_after();
-      uint32_t sr[128];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t t16[16];
-        tmem_ld16(tS + lane_off + c * 16, t16);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) sr[c * 16 + e] = t16[e];
-      }
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_free);
+      // pass 1: row max (TMEM re-read in pass 2 is cheaper than holding 128 registers)
       float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t t32[32];
+        tmem_ld32(tS + lane_off + c * 32, t32);
+        tmem_ld_wait();
 #pragma unroll
-      for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sr[e]));
+        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(t32[e]));
+      }
       mx *= p.scale_log2;
       // lazy rescale: only when the max grows by more than 2^8
       const bool need = (mx > m_used + 8.f);
@@ -213,36 +220,55 @@ __global__ void __launch_bounds__(192, 1)
         alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
         m_used = mx;
       }
-      float sum = 0.f;
       // P must not overwrite smem before PV_{j-1} has consumed it
       if (j > 0) {
         mbar_wait(o_done, (j - 1) & 1);
         tc_fence_after();
         if (__any_sync(0xffffffffu, need)) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o16[16];
-            tmem_ld16(tO + lane_off + c * 16, o16);
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            uint32_t o32[32];
+            tmem_ld32(tO + lane_off + c * 32, o32);
             tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) o16[e] = __float_as_uint(__uint_as_float(o16[e]) * alpha);
-            tmem_st16(tO + lane_off + c * 16, o16);
+            for (int e = 0; e < 32; ++e) o32[e] = __float_as_uint(__uint_as_float(o32[e]) * alpha);
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+                "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+                    tO + lane_off + c * 32),
+                "r"(o32[0]), "r"(o32[1]), "r"(o32[2]), "r"(o32[3]), "r"(o32[4]), "r"(o32[5]),
+                "r"(o32[6]), "r"(o32[7]), "r"(o32[8]), "r"(o32[9]), "r"(o32[10]), "r"(o32[11]),
+                "r"(o32[12]), "r"(o32[13]), "r"(o32[14]), "r"(o32[15]), "r"(o32[16]),
+                "r"(o32[17]), "r"(o32[18]), "r"(o32[19]), "r"(o32[20]), "r"(o32[21]),
+                "r"(o32[22]), "r"(o32[23]), "r"(o32[24]), "r"(o32[25]), "r"(o32[26]),
+                "r"(o32[27]), "r"(o32[28]), "r"(o32[29]), "r"(o32[30]), "r"(o32[31]));
           }
           tmem_st_wait();
         }
       }
       l *= alpha;
+      float sum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t t32[32];
+        tmem_ld32(tS + lane_off + c * 32, t32);
+        tmem_ld_wait();
+        if (c == 3) {   // S fully read: let the next S = Q K^T overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_free);
+        }
+        uint8_t* chunk = sP + (c >> 1) * FA_TILE;
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int t = 0; t < 4; ++t) {
           float pv[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            pv[e] = ex2(__uint_as_float(sr[ch * 64 + u * 8 + e]) * p.scale_log2 - m_used);
+            pv[e] = ex2(__uint_as_float(t32[t * 8 + e]) * p.scale_log2 - m_used);
             sum += pv[e];
           }
-          st_sw128(sP + ch * FA_TILE, r, u,
+          st_sw128(chunk, r, (c & 1) * 4 + t,
                    make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]),
                               pack_bf2(pv[4], pv[5]), pack_bf2(pv[6], pv[7])));
         }
@@ -301,7 +327,9 @@ struct FaBwdParams {
 // smem: K 16K | V 16K | Q[2] 32K | dO[2] 32K | P^T 32K | dS^T 32K | lse/D 2x2x512 | barriers
 constexpr int FA_BWD_SMEM = FA_TILE * 10 + 4096 + 1024 + 256;
 
-__global__ void __launch_bounds__(192, 1)
+constexpr int FA_BWD_THREADS = 320;   // TMA warp, MMA warp, 8 compute warps
+
+__global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                   const FaBwdParams p) {
@@ -345,10 +373,10 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(st_full, 1);
-    mbar_init(ps_full, 4);
+    mbar_init(ps_full, 8);
     mbar_init(mma_done, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_free, 4);
+    mbar_init(dq_free, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -428,12 +456,16 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
+    // 8 compute warps: lane quarter q = warp % 4 selects the TMEM lanes (key rows),
+    // `half` selects which 64 of the 128 query columns this warp processes.
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;                        // key row (S^T / dP^T lane)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float sl2 = p.scale * 1.4426950408889634f;
     for (int i = 0; i < n_q; ++i) {
       const int st = i & 1;
+      mbar_wait(&q_full[st], (i >> 1) & 1);   // lse / D of tile i visible
       mbar_wait(st_full, i & 1);
       tc_fence_after();
       // P^T / dS^T smem is free once the MMAs of tile i-1 completed
@@ -441,7 +473,8 @@ __global__ void __launch_bounds__(192, 1)
       const float* lse = sLse + st * 128;
       const float* dv = sD + st * 128;
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {          // 16 queries per chunk
+      for (int cc = 0; cc < 4; ++cc) {          // 16 queries per chunk
+        const int c = half * 4 + cc;
         uint32_t s16[16], d16[16];
         tmem_ld16(tSt + lane_off + c * 16, s16);
         tmem_ld16(tdPt + lane_off + c * 16, d16);
@@ -471,14 +504,14 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ps_full);
-      // dQ_i: this thread owns query row r of tile i
+      // dQ_i: this thread owns query row r of tile i, columns [half*32, half*32+32)
       mbar_wait(dq_full, i & 1);
       tc_fence_after();
-      float* dq = p.dQacc + (int64_t)(row0 + i * FA_BM + r) * p.ld + hh * FA_D;
+      float* dq = p.dQacc + (int64_t)(row0 + i * FA_BM + r) * p.ld + hh * FA_D + half * 32;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t t16[16];
-        tmem_ld16(tdQ + lane_off + c * 16, t16);
+        tmem_ld16(tdQ + lane_off + half * 32 + c * 16, t16);
         tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 16; e += 4)
@@ -491,29 +524,26 @@ __global__ void __launch_bounds__(192, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_free);
     }
-    // dK, dV epilogue: key row r
+    // dK (half 0) / dV (half 1) epilogue: key row r
     mbar_wait(mma_done, (n_q - 1) & 1);
     tc_fence_after();
     const int64_t grow = row0 + kt * FA_BN + r;
+    const uint32_t tacc = half ? tdV : tdK;
+    uint16_t* out = (half ? p.dV : p.dK) + grow * p.ld + hh * FA_D;
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tacc = which ? tdV : tdK;
-      uint16_t* out = (which ? p.dV : p.dK) + grow * p.ld + hh * FA_D;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t t16[16];
-        tmem_ld16(tacc + lane_off + c * 16, t16);
-        tmem_ld_wait();
-        uint4* dst = reinterpret_cast<uint4*>(out + c * 16);
-        dst[0] = make_uint4(pack_bf2(__uint_as_float(t16[0]), __uint_as_float(t16[1])),
-                            pack_bf2(__uint_as_float(t16[2]), __uint_as_float(t16[3])),
-                            pack_bf2(__uint_as_float(t16[4]), __uint_as_float(t16[5])),
-                            pack_bf2(__uint_as_float(t16[6]), __uint_as_float(t16[7])));
-        dst[1] = make_uint4(pack_bf2(__uint_as_float(t16[8]), __uint_as_float(t16[9])),
-                            pack_bf2(__uint_as_float(t16[10]), __uint_as_float(t16[11])),
-                            pack_bf2(__uint_as_float(t16[12]), __uint_as_float(t16[13])),
-                            pack_bf2(__uint_as_float(t16[14]), __uint_as_float(t16[15])));
-      }
+    for (int c = 0; c < 4; ++c) {
+      uint32_t t16[16];
+      tmem_ld16(tacc + lane_off + c * 16, t16);
+      tmem_ld_wait();
+      uint4* dst = reinterpret_cast<uint4*>(out + c * 16);
+      dst[0] = make_uint4(pack_bf2(__uint_as_float(t16[0]), __uint_as_float(t16[1])),
+                          pack_bf2(__uint_as_float(t16[2]), __uint_as_float(t16[3])),
+                          pack_bf2(__uint_as_float(t16[4]), __uint_as_float(t16[5])),
+                          pack_bf2(__uint_as_float(t16[6]), __uint_as_float(t16[7])));
+      dst[1] = make_uint4(pack_bf2(__uint_as_float(t16[8]), __uint_as_float(t16[9])),
+                          pack_bf2(__uint_as_float(t16[10]), __uint_as_float(t16[11])),
+                          pack_bf2(__uint_as_float(t16[12]), __uint_as_float(t16[13])),
+                          pack_bf2(__uint_as_float(t16[14]), __uint_as_float(t16[15])));
     }
   }
 
@@ -649,7 +679,7 @@ extern "C" int mp_attn_bwd(const void* q, const void* k, const void* v, const vo
   FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, scale, lse, dvec, dq_acc,
                 reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
   dim3 grid((unsigned)(s / FA_BN), (unsigned)(B * H));
-  fa_bwd_kernel<<<grid, 192, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, p);
+  fa_bwd_kernel<<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, p);
   MP_CHECK_LAUNCH();
   return 0;
 }

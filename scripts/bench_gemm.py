@@ -64,5 +64,27 @@ def main():
                       "mp_us": t * 1e6}), flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--attn" not in sys.argv:
     sys.exit(main())
+
+
+def bench_attention():
+    import math
+    B, H, s, d = 8, 32, 1024, 64
+    T = B * s
+    q, k, v, do = (torch.randn(T, H * d, device="cuda", dtype=torch.bfloat16) for _ in range(4))
+    o = torch.empty_like(q)
+    lse = torch.empty(B * H, s, device="cuda")
+    sc = 1 / math.sqrt(d)
+    t = timeit(lambda: native.attn_fwd(q, k, v, o, lse, B, H, s, d, sc))
+    fl = 4.0 * B * H * s * s * d
+    print(json.dumps({"shape": "attn_fwd", "tflops": fl / t / 1e12, "us": t * 1e6}), flush=True)
+    dvec = torch.empty(B * H, s, device="cuda")
+    dq = torch.zeros(T, H * d, device="cuda")
+    dk, dv = torch.empty_like(q), torch.empty_like(q)
+    t = timeit(lambda: native.attn_bwd(q, k, v, o, do, lse, dvec, dq, dk, dv, B, H, s, d, sc))
+    print(json.dumps({"shape": "attn_bwd", "tflops": 2.5 * fl / t / 1e12, "us": t * 1e6}), flush=True)
+
+
+if __name__ == "__main__" and "--attn" in sys.argv:
+    bench_attention()

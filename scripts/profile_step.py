@@ -22,6 +22,13 @@ def main():
     args = ap.parse_args()
     doc = json.loads(Path(args.plan).read_text())
     doc["num_microbatches"] = args.mb
+    import os
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        local = int(os.environ["LOCAL_RANK"])
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2201_12023_b200.runtime import Executor
     ex = Executor(doc, schedule="1f1b")
     ex.step()
@@ -38,10 +45,22 @@ def main():
                 name = "gemm " + name[name.find("<"):name.find(">") + 1] if "<" in name else name
             agg[name][0] += 1
             agg[name][1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
+    if world > 1 and dist.get_rank() != 0:
+        dist.barrier()
+        return
     total = sum(v[1] for v in agg.values())
     print(f"step device time {dt*1e3:.1f} ms, kernel sum {total/1e3:.1f} ms")
     for name, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:30]:
         print(f"{us/1e3:10.2f} ms {100*us/total:6.2f}% {n:7d}  {name[:110]}")
+    cpu = defaultdict(lambda: [0, 0.0])
+    for ev in prof.key_averages():
+        if ev.device_type == torch.autograd.DeviceType.CPU:
+            cpu[ev.key] = [ev.count, ev.self_cpu_time_total]
+    print("top CPU ops (self time):")
+    for name, (n, us) in sorted(cpu.items(), key=lambda kv: -kv[1][1])[:12]:
+        print(f"{us/1e3:10.2f} ms {n:7d}  {name[:100]}")
+    if world > 1:
+        dist.barrier()
 
 
 if __name__ == "__main__":
