@@ -71,9 +71,23 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// Store 8 bf16 (one 16-byte unit) of row r, unit u of a 128B-swizzled chunk.
+// Store 8 bf16 (one 16-byte unit) of row r, unit u of a 128B-swizzled chunk
+// (explicit st.shared: a generic store would go through the LSU's generic path).
 __device__ __forceinline__ void st_sw128(uint8_t* chunk, int r, int u, uint4 v) {
-  *reinterpret_cast<uint4*>(chunk + r * 128 + ((u ^ (r & 7)) << 4)) = v;
+  const uint32_t a = smem_u32(chunk) + r * 128 + ((u ^ (r & 7)) << 4);
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
 
 struct FaFwdParams {
@@ -404,8 +418,9 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       const int64_t base = (int64_t)bh * p.s + i * FA_BM;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        sLse[st * 128 + k * 32 + lane] = p.lse[base + k * 32 + lane];
-        sD[st * 128 + k * 32 + lane] = p.dvec[base + k * 32 + lane];
+        sts32(smem_u32(sLse + st * 128 + k * 32 + lane),
+              p.lse[base + k * 32 + lane] * 1.4426950408889634f);
+        sts32(smem_u32(sD + st * 128 + k * 32 + lane), p.dvec[base + k * 32 + lane]);
       }
       mbar_arrive(&q_full[st]);   // release semantics publish the lse / D stores
     }
@@ -470,21 +485,27 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       tc_fence_after();
       // P^T / dS^T smem is free once the MMAs of tile i-1 completed
       if (i > 0) mbar_wait(mma_done, (i - 1) & 1);
-      const float* lse = sLse + st * 128;
-      const float* dv = sD + st * 128;
+      const uint32_t lse_a = smem_u32(sLse + st * 128), d_a = smem_u32(sD + st * 128);
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {          // 16 queries per chunk
         const int c = half * 4 + cc;
         uint32_t s16[16], d16[16];
         tmem_ld16(tSt + lane_off + c * 16, s16);
         tmem_ld16(tdPt + lane_off + c * 16, d16);
+        float lse2[16], dvv[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 a = lds128(lse_a + (c * 16 + k * 4) * 4);
+          const float4 b = lds128(d_a + (c * 16 + k * 4) * 4);
+          lse2[4 * k] = a.x; lse2[4 * k + 1] = a.y; lse2[4 * k + 2] = a.z; lse2[4 * k + 3] = a.w;
+          dvv[4 * k] = b.x; dvv[4 * k + 1] = b.y; dvv[4 * k + 2] = b.z; dvv[4 * k + 3] = b.w;
+        }
         tmem_ld_wait();
         float pv[16], ds[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const int qq = c * 16 + e;
-          pv[e] = ex2(__uint_as_float(s16[e]) * sl2 - lse[qq] * 1.4426950408889634f);
-          ds[e] = pv[e] * (__uint_as_float(d16[e]) - dv[qq]) * p.scale;
+          pv[e] = ex2(fmaf(__uint_as_float(s16[e]), sl2, -lse2[e]));
+          ds[e] = pv[e] * (__uint_as_float(d16[e]) - dvv[e]) * p.scale;
         }
         const int ch = c >> 2, u0 = (c & 3) * 2;
         st_sw128(sPt + ch * FA_TILE, r, u0,
