@@ -13,6 +13,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <mutex>
+#include <cstdlib>
 #include "common.cuh"
 #include "../../include/mp_exec.h"
 
@@ -266,6 +267,236 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x BN tile.  Each CTA stages its own 128 rows of A and half (BN/2) of the
+// B columns; the leader (rank 0) issues tcgen05.mma.cta_group::2 with M = 256,
+// which reads both CTAs' shared memory and writes each CTA's 128 accumulator
+// rows into its own TMEM.  Per-CTA smem traffic per MMA drops to (4 + BN/32) KB
+// per 128*BN/256 cycles, and the 256-row tiles halve the wave count for the
+// N = 2048 projections of the GPT plans.
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;            // 128 rows of A
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;      // half of the B columns
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 6 : 8;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_2sm(const void* tmap, uint32_t bar_cluster, void* dst,
+                                                int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  using Cfg = Gemm2Cfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(Cfg::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int tiles_mn = p.tiles_m * p.tiles_n;   // tiles_m counts 256-row pair tiles
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs) {
+        const int b = t / tiles_mn;
+        const int rem = t - b * tiles_mn;
+        const int mb = rem / p.tiles_n;
+        const int nb = rem - mb * p.tiles_n;
+        const int b0 = b / p.nb1, b1 = b - (b / p.nb1) * p.nb1;
+        const int m0 = mb * 2 * BM + rank * BM;
+        const int n0 = nb * BN + rank * (BN / 2);
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+          uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
+          const int k0 = kb * BK;
+          if (p.a_mn) {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_4d_2sm(&tmA, fb, a_dst + i * 8192, m0 + 64 * i, k0, b1, b0);
+          } else {
+            tma_load_4d_2sm(&tmA, fb, a_dst, k0, m0, b1, b0);
+          }
+          if (p.b_mn) {
+#pragma unroll
+            for (int i = 0; i < BN / 128; ++i)
+              tma_load_4d_2sm(&tmB, fb, b_dst + i * 8192, n0 + 64 * i, k0, b1, b0);
+          } else {
+            tma_load_4d_2sm(&tmB, fb, b_dst, k0, n0, b1, b0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = umma_idesc_bf16(2 * BM, BN, p.a_mn, p.b_mn);
+      const uint32_t a_lbo = p.a_mn ? 8192u : 16u, b_lbo = p.b_mn ? 8192u : 16u;
+      const uint32_t a_kstep = p.a_mn ? 2048u : 32u, b_kstep = p.b_mn ? 2048u : 32u;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < p.num_tiles; t += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = umma_desc_sw128(a_base + kk * a_kstep, a_lbo, 1024u);
+            const uint64_t bd = umma_desc_sw128(b_base + kk * b_kstep, b_lbo, 1024u);
+            tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          tc_commit_2sm_mc(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_2sm_mc(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < p.num_tiles; t += npairs) {
+      const int b = t / tiles_mn;
+      const int rem = t - b * tiles_mn;
+      const int mb = rem / p.tiles_n;
+      const int nb = rem - mb * p.tiles_n;
+      const int b0 = b / p.nb1, b1 = b - (b / p.nb1) * p.nb1;
+      const int64_t row_off = (int64_t)b0 * p.c_bs0 + (int64_t)b1 * p.c_bs1;
+      const int m = mb * 2 * BM + rank * BM + row;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+        tmem_ld_wait();
+        const int n = nb * BN + c * 32;
+        if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(Cfg::TMEM_COLS)
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -339,6 +570,34 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams 
   return 0;
 }
 
+
+template <int BN>
+static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams p,
+                           cudaStream_t stream) {
+  using Cfg = Gemm2Cfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_2sm_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) {
+      set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      return 1;
+    }
+    configured = true;
+  }
+  p.tiles_m = (p.M + 2 * BM - 1) / (2 * BM);
+  p.tiles_n = (p.N + BN - 1) / BN;
+  p.num_tiles = p.tiles_m * p.tiles_n * p.nb0 * p.nb1;
+  int pairs = num_sms() / 2;
+  if (p.num_tiles < pairs) pairs = p.num_tiles;
+  gemm_bf16_2sm_kernel<BN><<<2 * pairs, kThreads, Cfg::SMEM, stream>>>(ma, mb, p);
+  return 0;
+}
+
+static int waves_x1000(int64_t tiles, int slots) {
+  const int64_t w = (tiles + slots - 1) / slots;
+  return (int)(1000 * w * slots / (tiles > 0 ? tiles : 1));
+}
 }  // namespace mp
 
 using namespace mp;
@@ -393,14 +652,26 @@ extern "C" int mp_gemm_bf16(const void* A, const int64_t* ad, const void* B, con
   }
   if (rc) return rc;
 
-  // B (K x N): MN-major if col stride 1, K-major if row stride 1.
-  int BN = (N > 128) ? 256 : (N > 64 ? 128 : 64);
+  // Tile shape: the 2-CTA kernel (256-row pair tiles) whenever M >= 256, with BN
+  // chosen to minimise wave-quantisation waste; else the 1-CTA kernel.
+  static const bool force_1sm = getenv("MPEXEC_GEMM_1SM") != nullptr;
+  const int64_t nb = nbatch0 * nbatch1;
+  static const int mode = getenv("MPEXEC_GEMM_2SM_BN") ? atoi(getenv("MPEXEC_GEMM_2SM_BN")) : 256;
+  bool two_sm = !force_1sm && M >= 256 && N >= 256;
+  int BN;
+  (void)nb;
+  if (two_sm) {
+    BN = mode == 128 ? 128 : 256;
+  } else {
+    BN = (N > 128) ? 256 : (N > 64 ? 128 : 64);
+  }
+  const int b_box_n = two_sm ? BN / 2 : BN;
   if (bd[3] == 1) {
     p.b_mn = 1;
     rc = make_map(&mb, B, N, K, bd[2], nbatch1, bd[5], nbatch0, bd[4], 64, BK);
   } else if (bd[2] == 1) {
     p.b_mn = 0;
-    rc = make_map(&mb, B, K, N, bd[3], nbatch1, bd[5], nbatch0, bd[4], BK, BN);
+    rc = make_map(&mb, B, K, N, bd[3], nbatch1, bd[5], nbatch0, bd[4], BK, b_box_n);
   } else {
     set_error("mp_gemm_bf16: B needs a unit stride");
     return 2;
@@ -408,7 +679,9 @@ extern "C" int mp_gemm_bf16(const void* A, const int64_t* ad, const void* B, con
   if (rc) return rc;
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (BN == 256)
+  if (two_sm)
+    rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, p, s) : launch_gemm_2sm<128>(ma, mb, p, s);
+  else if (BN == 256)
     rc = launch_gemm<256>(ma, mb, p, s);
   else if (BN == 128)
     rc = launch_gemm<128>(ma, mb, p, s);
