@@ -321,6 +321,25 @@ def attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, B: int, H: int, s: int
 
 # --------------------------------------------------------------------------- boxes
 
+def box_view(t: torch.Tensor, lo, ext) -> Optional[torch.Tensor]:
+    """Flat zero-copy view of box [lo, lo+ext) when it is one contiguous run of
+    a contiguous tensor (dims before the first partial dim have extent 1, dims
+    after it are full); else None.  Lets P2P send/recv skip pack/unpack."""
+    if not t.is_contiguous():
+        return None
+    shape = t.shape
+    k = 0
+    while k < len(shape) and ext[k] == 1:
+        k += 1
+    if any(ext[d] != shape[d] for d in range(k + 1, len(shape))):
+        return None
+    v = t
+    for d in range(len(shape)):
+        if lo[d] != 0 or ext[d] != shape[d]:
+            v = v.narrow(d, lo[d], ext[d])
+    return v.view(-1) if v.is_contiguous() else None
+
+
 def pack_box(src: torch.Tensor, lo, ext, out: Optional[torch.Tensor] = None,
              stream=None) -> torch.Tensor:
     """Dense copy of src[lo:lo+ext] (src any strided view, rank <= 4)."""

@@ -455,17 +455,23 @@ class StageRunner:
                 buf = native.pack_box(v, _lo(_rel(mv.box, mine)), _ext(mv.box))
                 native.unpack_box(buf, out, _lo(_rel(mv.box, want)), _ext(mv.box))
             elif mv.src == self.me:
-                sends.append((native.pack_box(v, _lo(_rel(mv.box, mine)), _ext(mv.box)), mv.dst))
+                lo, ext = _lo(_rel(mv.box, mine)), _ext(mv.box)
+                view = native.box_view(v, lo, ext)
+                sends.append((view if view is not None else native.pack_box(v, lo, ext), mv.dst))
             elif mv.dst == self.me:
-                buf = torch.empty(box_numel(mv.box), dtype=v.dtype, device=self.dev)
-                recvs.append((buf, mv.src, mv.box))
+                lo, ext = _lo(_rel(mv.box, want)), _ext(mv.box)
+                view = native.box_view(out, lo, ext)
+                buf = view if view is not None else torch.empty(box_numel(mv.box), dtype=v.dtype,
+                                                                device=self.dev)
+                recvs.append((buf, mv.src, lo, ext, view is None))
         if sends or recvs:
             grp = self.comm.stage_group(self.st.index, self.mesh)
-            works = self.comm.p2p(sends, [(b, s) for b, s, _ in recvs], grp)
+            works = self.comm.p2p(sends, [(b, s) for b, s, *_ in recvs], grp)
             for w in works:
                 w.wait()
-            for buf, _, box in recvs:
-                native.unpack_box(buf, out, _lo(_rel(box, want)), _ext(box))
+            for buf, _, lo, ext, packed in recvs:
+                if packed:
+                    native.unpack_box(buf, out, lo, ext)
         return out
 
     # ------------------------------------------------------------------ kernels
@@ -680,15 +686,19 @@ class StageRunner:
         recvs = []
         for k, t in recvs_of(bd, self.me):
             out, origin = outs[k]
-            buf = torch.empty(box_numel(t.box), dtype=torch.bfloat16, device=self.dev)
-            recvs.append((buf, t.src_device, out, _lo(_rel(t.box, origin)), _ext(t.box)))
+            lo, ext = _lo(_rel(t.box, origin)), _ext(t.box)
+            view = native.box_view(out, lo, ext)
+            buf = view if view is not None else torch.empty(box_numel(t.box), dtype=torch.bfloat16,
+                                                            device=self.dev)
+            recvs.append((buf, t.src_device, out, lo, ext, view is None))
         if recvs:
             works = self.comm.p2p([], [(b, s) for b, s, *_ in recvs],
                                   self.comm.boundary_group(bd, self.plan))
             for w in works:
                 w.wait()
-            for buf, _, out, lo, ext in recvs:
-                native.unpack_box(buf, out, lo, ext)
+            for buf, _, out, lo, ext, packed in recvs:
+                if packed:
+                    native.unpack_box(buf, out, lo, ext)
 
     def all_gather(self, ins: Instr):
         bd = ins.boundary
@@ -737,7 +747,9 @@ class StageRunner:
             node = self.graph[bt.node]
             v = self._as3(self.value(mb, bt.node))
             mine = _lo(device_box(node.dims, self.spec(bt.node), self.mesh, self.me))
-            sends.append((native.pack_box(v, _lo(_rel(t.box, mine)), _ext(t.box)), t.dst_device))
+            lo, ext = _lo(_rel(t.box, mine)), _ext(t.box)
+            view = native.box_view(v, lo, ext)
+            sends.append((view if view is not None else native.pack_box(v, lo, ext), t.dst_device))
         if sends:
             self.pending_sends += self.comm.p2p(sends, [], self.comm.boundary_group(bd, self.plan))
 
