@@ -81,11 +81,15 @@ int mp_sumsq(const void* x, float* out, int64_t n, void* stream);
 int mp_softmax_fwd(const void* x, void* y, int64_t rows, int64_t cols, int64_t ld,
                    float scale, void* stream);
 /* Split-row variant (softmax dim sharded over a mesh axis, SURVEY §7 hard
- * part 3): pass 1 writes per-row (max, sumexp) partials of the local columns;
- * after an all-reduce of the partials (max then rescaled sum), pass 2
- * normalises.  stats: fp32 [rows, 2]. */
+ * part 3).  stats: fp32 planar [3, rows] = (row max, row sum-exp, max copy).
+ *   mp_softmax_stats   local partials of the local columns
+ *   (caller: MAX all-reduce of stats[0:rows])
+ *   mp_softmax_rescale sum *= exp(local max - group max)
+ *   (caller: SUM all-reduce of stats[rows:2*rows])
+ *   mp_softmax_apply   y = exp(scale*x - max) / sum */
 int mp_softmax_stats(const void* x, float* stats, int64_t rows, int64_t cols,
                      int64_t ld, float scale, void* stream);
+int mp_softmax_rescale(float* stats, int64_t rows, void* stream);
 int mp_softmax_apply(const void* x, const float* stats, void* y, int64_t rows,
                      int64_t cols, int64_t ld, float scale, void* stream);
 /* dx = scale * y * (dy - rowsum(dy*y)); rowdot: optional fp32 [rows] holding

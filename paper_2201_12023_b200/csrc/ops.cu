@@ -213,10 +213,20 @@ __global__ void softmax_stats_kernel(const uint16_t* __restrict__ x, float* __re
   for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb) {
     float m, s;
     row_stats(x + r * ld, cols, scale, lane, m, s);
-    if (lane == 0) {
-      stats[2 * r] = m;
-      stats[2 * r + 1] = s;
+    if (lane == 0) {   // planar [3, rows]: max (all-reduced in place), sum, max copy
+      stats[r] = m;
+      stats[rows + r] = s;
+      stats[2 * rows + r] = m;
     }
+  }
+}
+
+// after the MAX all-reduce of stats[0]: rescale the local sums to the group max
+__global__ void softmax_rescale_kernel(float* __restrict__ stats, int64_t rows) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const float mg = stats[r], ml = stats[2 * rows + r];
+    stats[rows + r] = (ml == -INFINITY) ? 0.f : stats[rows + r] * __expf(ml - mg);
   }
 }
 
@@ -226,7 +236,7 @@ __global__ void softmax_apply_kernel(const uint16_t* __restrict__ x, const float
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb)
-    row_write(x + r * ld, y + r * ld, cols, scale, stats[2 * r], 1.f / stats[2 * r + 1], lane);
+    row_write(x + r * ld, y + r * ld, cols, scale, stats[r], 1.f / stats[rows + r], lane);
 }
 
 __device__ __forceinline__ float row_dot(const uint16_t* __restrict__ yr,
@@ -504,6 +514,15 @@ int mp_softmax_stats(const void* x, float* stats, int64_t rows, int64_t cols, in
   if (rows == 0) return 0;
   softmax_stats_kernel<<<row_grid(rows), 256, 0, MP_STREAM(stream)>>>((const uint16_t*)x, stats,
                                                                       rows, cols, ld, scale);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_softmax_rescale(float* stats, int64_t rows, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(stats && rows >= 0, "bad args");
+  if (rows == 0) return 0;
+  softmax_rescale_kernel<<<grid_for(rows, 256), 256, 0, MP_STREAM(stream)>>>(stats, rows);
   MP_CHECK_LAUNCH();
   return 0;
 }

@@ -113,3 +113,32 @@ def is_local_slice(dims, src: Spec, dst: Spec, mesh: Mesh, device: int) -> bool:
 
 def all_local(dims, src: Spec, dst: Spec, mesh: Mesh) -> bool:
     return all(is_local_slice(dims, src, dst, mesh, d) for d in mesh.device_ids)
+
+
+def allgather_axes(dims, have: Spec, req: Spec, mesh: Mesh) -> Optional[tuple[int, ...]]:
+    """Mesh axes A such that, on every device, the `req` tile is the dim-0
+    concatenation (in device-id order, i.e. NCCL group rank order) of the
+    `have` tiles of its A-axis group — then one all-gather into the output
+    realises the relayout (e.g. S^1R -> RR); None otherwise."""
+    found = None
+    for d in mesh.device_ids:
+        need = device_box(dims, req, mesh, d)
+        members = [e for e in sorted(mesh.device_ids)
+                   if _contains(need, device_box(dims, have, mesh, e))]
+        boxes = [device_box(dims, have, mesh, e) for e in members]
+        if len(members) < 2 or any(b[1:] != need[1:] for b in boxes):
+            return None
+        cut = need[0][0]
+        step = (need[0][1] - need[0][0]) // len(members)
+        for b in boxes:
+            if b[0] != (cut, cut + step):
+                return None
+            cut += step
+        if cut != need[0][1] or any(device_box(dims, req, mesh, e) != need for e in members):
+            return None
+        axes = next((ax for ax in ((0,), (1,), (0, 1)) if mesh.group_extent(ax) > 1
+                     and mesh.axis_group(d, ax) == tuple(members)), None)
+        if axes is None or (found is not None and axes != found):
+            return None
+        found = axes
+    return found

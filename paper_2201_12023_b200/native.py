@@ -36,6 +36,7 @@ EXPORTS = {
     "mp_sumsq": ([c_vp, c_vp, c_i64, c_vp], c_int),
     "mp_softmax_fwd": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
     "mp_softmax_stats": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
+    "mp_softmax_rescale": ([c_vp, c_i64, c_vp], c_int),
     "mp_softmax_apply": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
     "mp_softmax_bwd": ([c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
     "mp_softmax_rowdot": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp], c_int),
@@ -251,6 +252,12 @@ def softmax_stats(x: torch.Tensor, s: float, stats: torch.Tensor, stream=None) -
     rows, cols, ld = _rows(x, "x")
     _check(load().mp_softmax_stats(x.data_ptr(), stats.data_ptr(), rows, cols, ld, float(s),
                                    _stream(stream)), "mp_softmax_stats")
+    return stats
+
+
+def softmax_rescale(stats: torch.Tensor, rows: int, stream=None) -> torch.Tensor:
+    _require(stats, torch.float32, "stats")
+    _check(load().mp_softmax_rescale(stats.data_ptr(), rows, _stream(stream)), "mp_softmax_rescale")
     return stats
 
 

@@ -32,7 +32,8 @@ import torch.distributed as dist
 from . import native
 from .binding import Bound, bind
 from .comm import Comm
-from .layout import all_local, canonical, matmul_algo, relayout_moves, reshape_required
+from .layout import (all_local, allgather_axes, canonical, matmul_algo, relayout_moves,
+                     reshape_required)
 from .plan import (ExecPlan, Mesh, PlanError, Spec, box_numel, device_box, load_plan,
                    local_dims, replicated)
 from .schedule import GPIPE, Instr, Program, build_program
@@ -130,6 +131,7 @@ class StageRunner:
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self.cons = plan.graph.consumers()
         self._moves_cache: dict = {}
+        self._plans: dict = {}
         self._compile()
         self._init_params(params)
         self.step_count = 0
@@ -415,14 +417,41 @@ class StageRunner:
         if key in c:
             return c[key]
         dims = self.graph[nid].dims
-        if all_local(dims, have, req, self.mesh):
-            mine = device_box(dims, have, self.mesh, self.me)
-            want = device_box(dims, req, self.mesh, self.me)
-            out = self._narrow(v, [(lo - o, hi - lo) for (lo, hi), (o, _) in zip(want, mine)])
+        kind, info = self._relayout_plan(dims, have, req)
+        if kind == "local":
+            out = self._narrow(v, info)
+        elif kind == "allgather":
+            out = torch.empty(local_dims(dims, req, self.mesh), dtype=v.dtype, device=self.dev)
+            src = self._contig(self._as3(v))
+            self.comm.all_gather_into(out.view(-1), src.view(-1),
+                                      self.comm.axis_group(self.st.index, self.mesh, info, self.me))
         else:
             out = self._relayout(self._as3(v), dims, have, req)
         c[key] = out
         return out
+
+    def _relayout_plan(self, dims, have: Spec, req: Spec):
+        """How to realise `req` from `have` on this mesh (cached; decided from
+        every device's boxes, so all ranks of the stage agree):
+          local      every device's target box lies in its own tile: narrow
+          allgather  every device's target is the dim-0 concatenation, in
+                     device-id order, of the tiles of one axis group: one NCCL
+                     all-gather straight into the output
+          p2p        literal box moves (layout.relayout_moves) over NCCL P2P"""
+        key = (dims, have, req)
+        pl = self._plans.get(key)
+        if pl is not None:
+            return pl
+        m = self.mesh
+        if all_local(dims, have, req, m):
+            mine = device_box(dims, have, m, self.me)
+            want = device_box(dims, req, m, self.me)
+            pl = ("local", [(lo - o, hi - lo) for (lo, hi), (o, _) in zip(want, mine)])
+        else:
+            axes = allgather_axes(dims, have, req, m)
+            pl = ("allgather", axes) if axes is not None else ("p2p", None)
+        self._plans[key] = pl
+        return pl
 
     def _narrow(self, v: torch.Tensor, cuts) -> torch.Tensor:
         """Slice a local value by logical (offset, length) per dim; head-split
@@ -590,13 +619,11 @@ class StageRunner:
             if not split:
                 return native.softmax(x, s)
             rows = x.numel() // x.shape[-1]
-            stats = native.softmax_stats(x, s, torch.empty(rows, 2, dtype=torch.float32, device=self.dev))
-            mx = stats[:, 0].contiguous()
-            self._allreduce(mx, split, dist.ReduceOp.MAX)
-            z = (stats[:, 1] * torch.exp(stats[:, 0] - mx)).contiguous()
-            self._allreduce(z, split)
-            merged = torch.stack([mx, z], 1).contiguous()
-            return native.softmax_apply(x, merged, s)
+            stats = native.softmax_stats(x, s, torch.empty(3, rows, dtype=torch.float32, device=self.dev))
+            self._allreduce(stats[0], split, dist.ReduceOp.MAX)
+            native.softmax_rescale(stats, rows)
+            self._allreduce(stats[1], split)
+            return native.softmax_apply(x, stats, s)
         if k == "softmax_bwd":
             g, y = xs
             split = self._split_axes(op)

@@ -130,12 +130,16 @@ def test_softmax_split_rows():
     rows, cols, parts = 64, 1024, 4
     s = 0.125
     x = rnd(rows, cols, scale=3.0)
-    chunks = x.chunk(parts, dim=1)
-    stats = [native.softmax_stats(c.contiguous(), s, torch.empty(rows, 2, device="cuda")) for c in chunks]
-    m = torch.stack([st[:, 0] for st in stats]).max(0).values
-    z = sum(st[:, 1] * torch.exp(st[:, 0] - m) for st in stats)
-    merged = torch.stack([m, z], 1).contiguous()
-    y = torch.cat([native.softmax_apply(c.contiguous(), merged, s) for c in chunks], 1)
+    chunks = [c.contiguous() for c in x.chunk(parts, dim=1)]
+    stats = [native.softmax_stats(c, s, torch.empty(3, rows, device="cuda")) for c in chunks]
+    gmax = torch.stack([st[0] for st in stats]).max(0).values
+    for st in stats:                      # emulate the MAX all-reduce
+        st[0].copy_(gmax)
+        native.softmax_rescale(st, rows)
+    total = sum(st[1] for st in stats)    # emulate the SUM all-reduce
+    for st in stats:
+        st[1].copy_(total)
+    y = torch.cat([native.softmax_apply(c, st, s) for c, st in zip(chunks, stats)], 1)
     assert rel_err(y, torch.softmax(s * x.float(), -1)) < 1e-2
 
 

@@ -143,6 +143,28 @@ def test_relayout_moves_materialise_every_spec_pair(view):
             assert np.array_equal(got[d], glob[ir.sl(device_box(dims, dst, m, d))]), (src, dst, d)
 
 
+@pytest.mark.parametrize("view", [(1, 2), (2, 1), (2, 2), (1, 4), (2, 4), (4, 2), (1, 8)])
+def test_allgather_fast_path_is_exact(view):
+    """Whenever the all-gather fast path is taken, gathering the have-tiles of
+    the axis group in device-id order reproduces exactly the target tile."""
+    from oracle import ir
+    from paper_2201_12023_b200.layout import allgather_axes
+    m = mesh(view, 0)
+    dims = (8, 16)
+    glob = np.arange(np.prod(dims)).reshape(dims)
+    hits = 0
+    for src, dst in itertools.product(_all_specs(2, m, dims), repeat=2):
+        axes = allgather_axes(dims, src, dst, m)
+        if axes is None:
+            continue
+        hits += 1
+        for d in m.device_ids:
+            grp = m.axis_group(d, axes)
+            cat = np.concatenate([glob[ir.sl(device_box(dims, src, m, e))] for e in grp], 0)
+            assert np.array_equal(cat, glob[ir.sl(device_box(dims, dst, m, d))])
+    assert hits > 0
+
+
 def _all_specs(rank, m, dims):
     from paper_2201_12023_b200.plan import Spec
     out = set()
