@@ -62,6 +62,19 @@ int mp_gemm_bf16(const void* A, const int64_t* a_desc,
                  int64_t nbatch0, int64_t nbatch1,
                  float alpha, float beta, int epilogue,
                  void* stream);
+/* Same with fused epilogues on an auxiliary bf16 matrix (same M x N extents
+ * and batch structure as C; aux_desc = {row_stride, batch_stride0,
+ * batch_stride1}).  beta must be 0.
+ *   2: C = alpha*acc + aux            residual add / gradient accumulation
+ *                                     (the add member, graph.py:305,311,328-332)
+ *   3: C = alpha*acc * gelu'(aux)     GeLU backward on the dX of the next matmul
+ *   4: C = alpha*acc; aux <- gelu(C)  pre-activation and activation in one pass */
+int mp_gemm_bf16_ex(const void* A, const int64_t* a_desc,
+                    const void* B, const int64_t* b_desc,
+                    void* C, const int64_t* c_desc, int c_dtype,
+                    int64_t nbatch0, int64_t nbatch1,
+                    float alpha, float beta, int epilogue,
+                    void* aux, const int64_t* aux_desc, void* stream);
 
 /* ---- elementwise / row ops (trivial members, intra.py:93-160) ------------- */
 

@@ -21,7 +21,7 @@ namespace mp {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 8;   // two warps per TMEM lane quarter, each half the columns
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 struct GemmParams {
@@ -33,7 +33,9 @@ struct GemmParams {
   int64_t ldc, c_bs0, c_bs1;
   int c_f32;
   float alpha, beta;
-  int epi;
+  int epi;            // 0 none, 1 gelu, 2 +aux, 3 *gelu'(aux), 4 C=pre & aux:=gelu(pre)
+  uint16_t* aux;      // bf16 (M x N) with row stride aux_ld (input for 2/3, output for 4)
+  int64_t aux_ld, aux_bs0, aux_bs1;
 };
 
 template <int BN>
@@ -48,7 +50,7 @@ struct GemmCfg {
 
 template <int BN>
 __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off, int m, int n,
-                                            const uint32_t (&r)[32]) {
+                                            const uint32_t (&r)[32], int b0 = 0, int b1 = 0) {
   // r: 32 consecutive fp32 accumulator columns [n, n+32) of row m
   float v[32];
 #pragma unroll
@@ -56,6 +58,46 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off
   if (p.epi == 1) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+  } else if (p.epi >= 2) {
+    uint16_t* ax = p.aux + (int64_t)b0 * p.aux_bs0 + (int64_t)b1 * p.aux_bs1 +
+                   (int64_t)m * p.aux_ld + n;
+    if (p.epi == 4) {      // dual output: aux <- gelu(pre), C <- pre
+      if (n + 32 <= p.N) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<uint4*>(ax)[i] = make_uint4(
+              pack_bf2(gelu_tanh(v[8 * i]), gelu_tanh(v[8 * i + 1])),
+              pack_bf2(gelu_tanh(v[8 * i + 2]), gelu_tanh(v[8 * i + 3])),
+              pack_bf2(gelu_tanh(v[8 * i + 4]), gelu_tanh(v[8 * i + 5])),
+              pack_bf2(gelu_tanh(v[8 * i + 6]), gelu_tanh(v[8 * i + 7])));
+      } else {
+        for (int i = 0; i < 32 && n + i < p.N; ++i) ax[i] = f2bf(gelu_tanh(v[i]));
+      }
+    } else {
+      float a[32];
+      if (n + 32 <= p.N) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 u = reinterpret_cast<const uint4*>(ax)[i];
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            a[8 * i + 2 * j] = bf2f(w[j] & 0xffff);
+            a[8 * i + 2 * j + 1] = bf2f(w[j] >> 16);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) a[i] = (n + i < p.N) ? bf2f(ax[i]) : 0.f;
+      }
+      if (p.epi == 2) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += a[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= gelu_tanh_grad(a[i]);
+      }
+    }
   }
   const bool full = (n + 32 <= p.N);
   if (p.c_f32) {
@@ -229,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // epilogue warps: TMEM lane quarter is fixed by (warp % 4)
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -243,12 +286,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         const int n = nb * BN + c * 32;
-        if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r);
+        if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r, b0, b1);
       }
       tc_fence_before();
       __syncwarp();
@@ -455,6 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = q * 32 + lane;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
@@ -471,12 +515,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         const int n = nb * BN + c * 32;
-        if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r);
+        if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r, b0, b1);
       }
       tc_fence_before();
       __syncwarp();
@@ -602,10 +646,23 @@ static int waves_x1000(int64_t tiles, int slots) {
 
 using namespace mp;
 
+extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
+                               const int64_t* bd, void* C, const int64_t* cd, int c_dtype,
+                               int64_t nbatch0, int64_t nbatch1, float alpha, float beta,
+                               int epilogue, void* aux, const int64_t* aux_desc, void* stream);
+
 extern "C" int mp_gemm_bf16(const void* A, const int64_t* ad, const void* B, const int64_t* bd,
                             void* C, const int64_t* cd, int c_dtype, int64_t nbatch0,
                             int64_t nbatch1, float alpha, float beta, int epilogue,
                             void* stream) {
+  return mp_gemm_bf16_ex(A, ad, B, bd, C, cd, c_dtype, nbatch0, nbatch1, alpha, beta, epilogue,
+                         nullptr, nullptr, stream);
+}
+
+extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
+                               const int64_t* bd, void* C, const int64_t* cd, int c_dtype,
+                               int64_t nbatch0, int64_t nbatch1, float alpha, float beta,
+                               int epilogue, void* aux, const int64_t* aux_desc, void* stream) {
   clear_error();
   MP_CHECK_ARG(A && B && C && ad && bd && cd, "null argument");
   const int64_t M = ad[0], K = ad[1], N = bd[1];
@@ -615,7 +672,11 @@ extern "C" int mp_gemm_bf16(const void* A, const int64_t* ad, const void* B, con
   MP_CHECK_ARG(M < (1LL << 31) && N < (1LL << 31) && K < (1LL << 31), "gemm dims too large");
   MP_CHECK_ARG(cd[3] == 1, "C must have unit column stride");
   MP_CHECK_ARG(c_dtype == 0 || c_dtype == 1, "c_dtype must be 0 (bf16) or 1 (f32)");
-  MP_CHECK_ARG(epilogue == 0 || (epilogue == 1 && beta == 0.f), "bad epilogue");
+  MP_CHECK_ARG(epilogue >= 0 && epilogue <= 4, "bad epilogue");
+  MP_CHECK_ARG(epilogue == 0 || beta == 0.f, "fused epilogues require beta == 0");
+  MP_CHECK_ARG(epilogue < 2 || (aux && aux_desc && reinterpret_cast<uintptr_t>(aux) % 16 == 0 &&
+                                aux_desc[0] % 8 == 0),
+               "epilogues 2-4 need a 16-byte aligned bf16 aux matrix with 8-element rows");
   MP_CHECK_ARG(nbatch0 >= 1 && nbatch1 >= 1, "bad batch extents");
   MP_CHECK_ARG(reinterpret_cast<uintptr_t>(C) % 16 == 0 && cd[2] % (c_dtype ? 4 : 8) == 0,
                "C must be 16-byte aligned with 16-byte aligned rows");
@@ -636,6 +697,12 @@ extern "C" int mp_gemm_bf16(const void* A, const int64_t* ad, const void* B, con
   p.alpha = alpha;
   p.beta = beta;
   p.epi = epilogue;
+  p.aux = reinterpret_cast<uint16_t*>(aux);
+  if (epilogue >= 2) {
+    p.aux_ld = aux_desc[0];
+    p.aux_bs0 = aux_desc[1];
+    p.aux_bs1 = aux_desc[2];
+  }
 
   // A (M x K): K-major if col stride 1, else MN-major (row stride 1).
   CUtensorMap ma, mb;

@@ -29,6 +29,8 @@ EXPORTS = {
     "mp_launch_count": ([], ctypes.c_uint64),
     "mp_gemm_bf16": ([c_vp, c_i64p, c_vp, c_i64p, c_vp, c_i64p, c_int, c_i64, c_i64,
                       c_f32, c_f32, c_int, c_vp], c_int),
+    "mp_gemm_bf16_ex": ([c_vp, c_i64p, c_vp, c_i64p, c_vp, c_i64p, c_int, c_i64, c_i64,
+                         c_f32, c_f32, c_int, c_vp, c_i64p, c_vp], c_int),
     "mp_gelu_fwd": ([c_vp, c_vp, c_i64, c_vp], c_int),
     "mp_gelu_bwd": ([c_vp, c_vp, c_vp, c_i64, c_vp], c_int),
     "mp_add": ([c_vp, c_vp, c_vp, c_i64, c_vp], c_int),
@@ -133,11 +135,17 @@ def _split_batch(t: torch.Tensor, name: str):
 gemm_timer: Optional[list] = None
 
 
+EPI_NONE, EPI_GELU, EPI_ADD, EPI_GELU_GRAD, EPI_GELU_DUAL = 0, 1, 2, 3, 4
+
+
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 1.0,
-         beta: float = 0.0, gelu: bool = False, stream=None) -> torch.Tensor:
-    """out = alpha * a @ b + beta * out on the tcgen05 kernel.  a: (…, M, K),
+         beta: float = 0.0, gelu: bool = False, epilogue: int = 0,
+         aux: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """out = epi(alpha * a @ b + beta * out) on the tcgen05 kernel.  a: (…, M, K),
     b: (…, K, N) bf16 views (any of K-/MN-major), out: (…, M, N) bf16 or fp32
-    with unit column stride.  Batch dims must agree."""
+    with unit column stride.  Batch dims must agree.  epilogue (see
+    include/mp_exec.h): EPI_ADD / EPI_GELU_GRAD read `aux`, EPI_GELU_DUAL
+    writes gelu(out) into `aux`; aux has out's shape, bf16, unit column stride."""
     _require(a, torch.bfloat16, "a")
     _require(b, torch.bfloat16, "b")
     if out.dtype not in (torch.bfloat16, torch.float32):
@@ -147,16 +155,26 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
     cd, cb = _split_batch(out, "out")
     if not (ab == bb == cb):
         raise NativeError(f"batch mismatch {ab} {bb} {cb}")
+    epi = 1 if gelu else int(epilogue)
+    aux_ptr, aux_desc = None, None
+    if epi >= 2:
+        if aux is None:
+            raise NativeError("epilogue needs aux")
+        _require(aux, torch.bfloat16, "aux")
+        xd, xb = _split_batch(aux, "aux")
+        if xb != cb or xd[0] != cd[0] or xd[1] != cd[1] or xd[3] != 1:
+            raise NativeError("aux must match out's shape with unit column stride")
+        aux_ptr, aux_desc = aux.data_ptr(), _arr([xd[2], xd[4], xd[5]])
     st = _stream(stream)
     timer = gemm_timer
     if timer is not None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-    rc = load().mp_gemm_bf16(a.data_ptr(), _arr(ad), b.data_ptr(), _arr(bd), out.data_ptr(),
-                             _arr(cd), 1 if out.dtype == torch.float32 else 0, ab[0], ab[1],
-                             float(alpha), float(beta), 1 if gelu else 0, st)
-    _check(rc, "mp_gemm_bf16")
+    rc = load().mp_gemm_bf16_ex(a.data_ptr(), _arr(ad), b.data_ptr(), _arr(bd), out.data_ptr(),
+                                _arr(cd), 1 if out.dtype == torch.float32 else 0, ab[0], ab[1],
+                                float(alpha), float(beta), epi, aux_ptr, aux_desc, st)
+    _check(rc, "mp_gemm_bf16_ex")
     if timer is not None:
         e1.record()
         timer.append((2.0 * ad[0] * ad[1] * bd[1] * ab[0] * ab[1], e0, e1))

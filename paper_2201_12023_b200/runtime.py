@@ -90,7 +90,7 @@ def _rel(box, origin):
 
 
 class _Op:
-    __slots__ = ("nid", "op", "bound", "ins", "out_spec", "algo", "grad_direct", "extra")
+    __slots__ = ("nid", "op", "bound", "ins", "out_spec", "algo", "grad_direct", "extra", "epi")
 
     def __init__(self, nid, op, bound, ins, out_spec, algo=None):
         self.nid = nid
@@ -101,6 +101,7 @@ class _Op:
         self.algo = algo
         self.grad_direct = False         # dW accumulated straight into the fp32 grad buffer
         self.extra = None
+        self.epi = None                  # fused GEMM epilogue (kind, consumer, aux node)
 
 
 class StageRunner:
@@ -209,6 +210,51 @@ class StageRunner:
         self.members = members
         self.fuse_attention = os.environ.get("MPEXEC_FUSE_ATTENTION", "1") != "0"
         self.attn_clusters = self._fuse_attention() if self.fuse_attention else []
+        self.fused_epilogues = (self._fuse_epilogues()
+                                if os.environ.get("MPEXEC_FUSE_EPILOGUE", "1") != "0" else 0)
+
+    def _fuse_epilogues(self) -> int:
+        """Fold a matmul's single trivial consumer into its GEMM epilogue:
+        gelu (dual output: pre-activation + activation), gelu_bwd (dX * gelu'),
+        add (residual / gradient accumulation).  Only when no relayout or
+        all-reduce sits between them (same spec, no k-split) and the matmul's
+        own value is not needed elsewhere.  Returns the number fused."""
+        refs = {op.bound.fwd_ref for op in self.fwd_ops + self.bwd_ops if op.bound.fwd_ref is not None}
+        n = 0
+        for name in ("fwd_ops", "bwd_ops"):
+            ops = getattr(self, name)
+            pos = {o.nid: i for i, o in enumerate(ops)}
+            removed = set()
+            for i, o in enumerate(ops):
+                if o.op != "matmul" or o.grad_direct or o.algo.k_axes or o.epi is not None \
+                        or o.nid in self.st.output_specs:
+                    continue
+                users = self.cons[o.nid]
+                if len(users) != 1 or users[0][0] not in pos or users[0][0] in removed:
+                    continue
+                u = users[0][0]
+                uop = ops[pos[u]]
+                if self.spec(u) != o.out_spec:
+                    continue
+                if uop.op == "gelu":
+                    o.epi = ("dual", u, None)
+                elif uop.op == "gelu_bwd" and o.nid not in refs:
+                    x_ref = uop.bound.fwd_ref
+                    if uop.ins[0][0] != o.nid or self.spec(x_ref) != o.out_spec:
+                        continue
+                    o.epi = ("gelu_grad", u, x_ref)
+                elif uop.op == "add" and o.nid not in refs:
+                    others = [p for p, _ in uop.ins if p != o.nid]
+                    if len(others) != 1 or pos.get(others[0], -1) > i \
+                            or self.spec(others[0]) != o.out_spec:
+                        continue
+                    o.epi = ("add", u, others[0])
+                else:
+                    continue
+                removed.add(u)
+                n += 1
+            setattr(self, name, [o for o in ops if o.nid not in removed])
+        return n
 
     # ------------------------------------------------------------------ fusion
     def _fuse_attention(self) -> list[dict]:
@@ -535,6 +581,20 @@ class StageRunner:
             self._gemm(a, b, out_view, beta=1.0)
             return None
         shape = tuple(a.shape[:-2]) + (a.shape[-2], b.shape[-1])
+        if op.epi is not None:
+            kind, u, aux_nid = op.epi
+            out = torch.empty(shape, dtype=torch.bfloat16, device=self.dev)
+            vals = self.vals[mb]
+            if kind == "dual":
+                act = torch.empty_like(out)
+                self._gemm(a, b, out, epilogue=native.EPI_GELU_DUAL, aux=act)
+                vals[u] = act
+                return out
+            aux = self._contig(self._as3(self.get(mb, aux_nid, op.out_spec)))
+            self._gemm(a, b, out, epilogue=native.EPI_GELU_GRAD if kind == "gelu_grad"
+                       else native.EPI_ADD, aux=aux)
+            vals[u] = out
+            return None
         if op.extra is not None and not k_axes:
             # the only consumer is a head merge: write straight into (T, h) layout
             kind, (B, H, s, d) = op.extra
@@ -554,11 +614,13 @@ class StageRunner:
             out = out.view(out.shape[0] * out.shape[1], *out.shape[2:])
         return out
 
-    def _gemm(self, a, b, out, beta=0.0):
+    def _gemm(self, a, b, out, beta=0.0, epilogue=0, aux=None):
         if out.stride(-1) != 1 and out.stride(-2) == 1:
+            if epilogue:
+                raise ExecError("fused epilogues need a row-major output")
             native.gemm(b.transpose(-1, -2), a.transpose(-1, -2), out.transpose(-1, -2), beta=beta)
         else:
-            native.gemm(a, b, out, beta=beta)
+            native.gemm(a, b, out, beta=beta, epilogue=epilogue, aux=aux)
 
     def _run_reshape(self, mb: int, op: _Op) -> torch.Tensor:
         x = self.get(mb, op.ins[0][0], op.ins[0][1])

@@ -64,7 +64,7 @@ def main():
                       "mp_us": t * 1e6}), flush=True)
 
 
-if __name__ == "__main__" and "--attn" not in sys.argv:
+if __name__ == "__main__" and "--attn" not in sys.argv and "--epi" not in sys.argv:
     sys.exit(main())
 
 
@@ -88,3 +88,22 @@ def bench_attention():
 
 if __name__ == "__main__" and "--attn" in sys.argv:
     bench_attention()
+
+
+def bench_epilogues():
+    M, K = 8192, 2048
+    for name, N, K2, epi in (("mlp_up+gelu_dual", 8192, 2048, native.EPI_GELU_DUAL),
+                             ("proj+add", 2048, 2048, native.EPI_ADD),
+                             ("mlp_down+add", 2048, 8192, native.EPI_ADD),
+                             ("dX_mlp2+gelu_grad", 8192, 2048, native.EPI_GELU_GRAD),
+                             ("mlp_up plain", 8192, 2048, 0)):
+        a = torch.randn(M, K2, device="cuda", dtype=torch.bfloat16)
+        b = torch.randn(K2, N, device="cuda", dtype=torch.bfloat16)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        aux = torch.randn(M, N, device="cuda", dtype=torch.bfloat16)
+        t = timeit(lambda: native.gemm(a, b, out, epilogue=epi, aux=aux if epi else None))
+        print(json.dumps({"shape": name, "tflops": 2.0 * M * N * K2 / t / 1e12, "us": t * 1e6}), flush=True)
+
+
+if __name__ == "__main__" and "--epi" in sys.argv:
+    bench_epilogues()

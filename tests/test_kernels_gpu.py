@@ -182,3 +182,21 @@ def test_launch_counter_advances():
     c0 = native.launch_count()
     native.gelu(rnd(64))
     assert native.launch_count() == c0 + 1
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (1000, 520, 136), (128, 256, 64)])
+def test_gemm_fused_epilogues(M, N, K):
+    a, b = rnd(M, K), rnd(K, N, scale=0.1)
+    acc = a.float() @ b.float()
+    aux = rnd(M, N)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    native.gemm(a, b, out, epilogue=native.EPI_ADD, aux=aux)
+    assert rel_err(out, acc + aux.float()) < 1e-2
+    native.gemm(a, b, out, epilogue=native.EPI_GELU_GRAD, aux=aux)
+    xf = aux.float().requires_grad_()
+    torch.nn.functional.gelu(xf, approximate="tanh").backward(acc)
+    assert rel_err(out, xf.grad) < 1e-2
+    act = torch.empty_like(out)
+    native.gemm(a, b, out, epilogue=native.EPI_GELU_DUAL, aux=act)
+    assert rel_err(out, acc) < 1e-2
+    assert rel_err(act, torch.nn.functional.gelu(acc, approximate="tanh")) < 1e-2
