@@ -133,6 +133,9 @@ class StageRunner:
         self.cons = plan.graph.consumers()
         self._moves_cache: dict = {}
         self._plans: dict = {}
+        self.dw_stream = (torch.cuda.Stream() if os.environ.get("MPEXEC_DW_STREAM", "1") != "0"
+                          else None)
+        self.dw_pending = False
         self._compile()
         self._init_params(params)
         self.step_count = 0
@@ -576,9 +579,20 @@ class StageRunner:
         a, b = self._gemm_operands(a, b)
         k_axes = op.algo.k_axes
         if op.grad_direct:
+            # dW only feeds the step-end reduction: run it on a side stream so it
+            # overlaps the dX chain and fills the other GEMMs' tail waves
             gv = self.gviews[op.nid]
             out_view = gv if a.dim() == 2 else gv.view(*a.shape[:-2], a.shape[-2], b.shape[-1])
-            self._gemm(a, b, out_view, beta=1.0)
+            main = torch.cuda.current_stream()
+            if self.dw_stream is None:
+                self._gemm(a, b, out_view, beta=1.0)
+                return None
+            self.dw_stream.wait_stream(main)
+            with torch.cuda.stream(self.dw_stream):
+                self._gemm(a, b, out_view, beta=1.0)
+            a.record_stream(self.dw_stream)
+            b.record_stream(self.dw_stream)
+            self.dw_pending = True
             return None
         shape = tuple(a.shape[:-2]) + (a.shape[-2], b.shape[-1])
         if op.epi is not None:
@@ -849,12 +863,18 @@ class StageRunner:
             self.aux.pop(ins.microbatch, None)
 
     # ------------------------------------------------------------------ optimizer
+    def join_dw(self):
+        if self.dw_stream is not None and self.dw_pending:
+            torch.cuda.current_stream().wait_stream(self.dw_stream)
+            self.dw_pending = False
+
     def reduce_grads(self):
         """Finish the gradient of every parameter: all-reduce the k-split partial
         sums accumulated over the microbatches (sharding.py:284-291; one reduction
         per step instead of per microbatch, the sum is linear) and move them to
         the parameter's layout."""
         g = self.graph
+        self.join_dw()
         for pid in self.param_ids:
             dw = self.grad_nodes.get(pid)
             if dw is None:
@@ -882,6 +902,7 @@ class StageRunner:
         self.apply_update()
 
     def zero_grads(self):
+        self.join_dw()
         self.gradbuf.zero_()
         for dw, gv in self.gviews.items():
             if gv.data_ptr() < self.gradbuf.data_ptr() or \
@@ -925,6 +946,7 @@ class StageRunner:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
                 events.append((ins, e0, e1))
+        self.join_dw()
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(stream)
         return t0, t1, events
