@@ -233,6 +233,21 @@ def main():
     g_flop = sum(f for f, _, _ in timer)
     g_time = sum(a.elapsed_time(b) for _, a, b in timer) * 1e-3
     g_n = len(timer)
+    # dW GEMMs run on a side stream and overlap the dX chain, so per-launch
+    # durations overlap too: the roofline uses the union of the GEMM intervals
+    # (device time during which at least one GEMM ran).
+    iv = sorted((ev0.elapsed_time(a), ev0.elapsed_time(b)) for _, a, b in timer)
+    g_union, cur_s, cur_e = 0.0, None, None
+    for a_, b_ in iv:
+        if cur_e is None or a_ > cur_e:
+            if cur_e is not None:
+                g_union += cur_e - cur_s
+            cur_s, cur_e = a_, b_
+        else:
+            cur_e = max(cur_e, b_)
+    if cur_e is not None:
+        g_union += cur_e - cur_s
+    g_union *= 1e-3
 
     # ---- e2e through the public API: H2D inputs from pinned host, D2H loss
     e2e = None
@@ -261,7 +276,7 @@ def main():
             dist.destroy_process_group()
         return 0
     sus, burst, hbm, src = peaks()
-    ach = g_flop / g_time / 1e12 if g_time > 0 else 0.0
+    ach = g_flop / g_union / 1e12 if g_union > 0 else 0.0
     out = {
         "metric": METRIC, "value": step_flop / t / 1e12, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -274,7 +289,8 @@ def main():
                      "frac": ach / sus, "traffic": None,
                      "kernel": "mp::gemm_bf16_kernel (tcgen05)",
                      "launches": g_n, "avg_launch_us": g_time / max(g_n, 1) * 1e6,
-                     "gemm_share_of_step": g_time / (t_local) if t_local else None,
+                     "achieved_basis": "GEMM FLOPs / union of GEMM launch intervals (CUDA events)",
+                     "gemm_share_of_step": g_union / t_local if t_local else None,
                      "peak_source": f"{src} bf16_tflops_sustained"},
         "gpu_launches": launches // args.steps,
         "loss": loss,
