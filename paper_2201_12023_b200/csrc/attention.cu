@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(192, 2)
 
 // ------------------------------------------------------------------ backward
 struct FaBwdParams {
+  int* status;        // set to 1 if the kernel could not run (smem misaligned)
   int B, H, s, ld;
   float scale;        // 1/sqrt(d)
   const float* lse;   // [B*H, s]
@@ -338,35 +339,42 @@ struct FaBwdParams {
   uint16_t* dV;
 };
 
-// smem: K 16K | V 16K | Q[2] 32K | dO[2] 32K | P^T 32K | dS^T 32K | lse/D 2x2x512 | barriers
-constexpr int FA_BWD_SMEM = FA_TILE * 10 + 4096 + 1024 + 256;
-
-constexpr int FA_BWD_THREADS = 320;   // TMA warp, MMA warp, 8 compute warps
+// smem: K 16K | V 16K | Q[2] 32K | dO[2] 32K | P^T[2] 64K | dS^T[2] 64K | barriers (224 KB)
+// P^T / dS^T are double-buffered so the P/dS math of query tile i overlaps the
+// dV / dK / dQ MMAs of tile i-1; LSE / D are read straight from global (L1-broadcast).
+// (no alignment slack: the dynamic smem window of a cluster-less CTA is 1 KB
+// aligned on sm_100; the kernel checks it and reports instead of corrupting)
+constexpr int FA_BWD_SMEM = FA_TILE * 14 + 2048 + 256;
+constexpr int FA_BWD_THREADS = 448;   // TMA, MMA, 8 P/dS warps, 4 dQ warps
 
 __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                   const FaBwdParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (smem_u32(smem_raw) & 1023) {
+    if (threadIdx.x == 0) atomicExch(p.status, 1);
+    return;
+  }
+  uint8_t* smem = smem_raw;
   uint8_t* sK = smem;
   uint8_t* sV = smem + FA_TILE;
   uint8_t* sQ = smem + 2 * FA_TILE;    // [2]
   uint8_t* sdO = smem + 4 * FA_TILE;   // [2]
-  uint8_t* sPt = smem + 6 * FA_TILE;   // 2 chunks (queries 0-63 | 64-127)
-  uint8_t* sdSt = smem + 8 * FA_TILE;  // 2 chunks
-  float* sLse = reinterpret_cast<float*>(smem + 10 * FA_TILE);   // [2][128]
+  uint8_t* sPt = smem + 6 * FA_TILE;   // [2] x 2 chunks (queries 0-63 | 64-127)
+  uint8_t* sdSt = smem + 10 * FA_TILE; // [2] x 2 chunks
+  float* sLse = reinterpret_cast<float*>(smem + 14 * FA_TILE);   // [2][128], log2 domain
   float* sD = sLse + 256;                                        // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 10 * FA_TILE + 4096);
-  uint64_t* kv_full = bars;         // K, V
-  uint64_t* q_full = bars + 1;      // [2] Q_i, dO_i (+ lse/D via the producer warp)
-  uint64_t* q_empty = bars + 3;     // [2]
-  uint64_t* st_full = bars + 5;     // S^T and dP^T in TMEM
-  uint64_t* ps_full = bars + 6;     // P^T / dS^T in smem (4 warps)
-  uint64_t* mma_done = bars + 7;    // dV/dK/dQ MMAs of tile i finished (smem free)
-  uint64_t* dq_full = bars + 8;
-  uint64_t* dq_free = bars + 9;     // 4 warps
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 14 * FA_TILE + 2048);
+  uint64_t* kv_full = bars;          // K, V
+  uint64_t* q_full = bars + 1;       // [2] Q_i, dO_i
+  uint64_t* q_empty = bars + 3;      // [2]
+  uint64_t* st_full = bars + 5;      // S^T and dP^T of tile i in TMEM
+  uint64_t* ps_full = bars + 6;      // P^T / dS^T of tile i in smem (8 warps)
+  uint64_t* pbuf_free = bars + 7;    // [2] MMAs of a tile done with its P^T / dS^T buffer
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_free = bars + 10;     // 4 dQ warps
+  uint64_t* acc_done = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -383,14 +391,15 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     tma_prefetch(&tmdO);
     mbar_init(kv_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1 + 32);   // tx arrive + 32 lanes copying lse / D
+      mbar_init(&q_full[i], 1 + 32);   // tx arrive + 32 lanes staging lse / D
       mbar_init(&q_empty[i], 1);
+      mbar_init(&pbuf_free[i], 1);
     }
     mbar_init(st_full, 1);
     mbar_init(ps_full, 8);
-    mbar_init(mma_done, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_free, 8);
+    mbar_init(dq_free, 4);
+    mbar_init(acc_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -422,7 +431,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
               p.lse[base + k * 32 + lane] * 1.4426950408889634f);
         sts32(smem_u32(sD + st * 128 + k * 32 + lane), p.dvec[base + k * 32 + lane]);
       }
-      mbar_arrive(&q_full[st]);   // release semantics publish the lse / D stores
+      mbar_arrive(&q_full[st]);   // release: publishes the lse / D stores
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -430,12 +439,34 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       const uint32_t id_acc = umma_idesc_bf16(128, 64, 0, 1);  // P^T/dS^T (K-major) x dO/Q (MN)
       const uint32_t id_dq = umma_idesc_bf16(128, 64, 1, 1);   // dS (MN-major) x K (MN-major)
       const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
-      const uint32_t pt_base = smem_u32(sPt), dst_base = smem_u32(sdSt);
+      // dV/dK/dQ of tile j (operands: P^T/dS^T buffer j&1, Q/dO stage j&1)
+      auto issue_acc = [&](int j) {
+        const int bj = j & 1;
+        const uint32_t pt = smem_u32(sPt + bj * 2 * FA_TILE), ds = smem_u32(sdSt + bj * 2 * FA_TILE);
+        const uint32_t qb = smem_u32(sQ + bj * FA_TILE), dob = smem_u32(sdO + bj * FA_TILE);
+#pragma unroll
+        for (int kk = 0; kk < FA_BM / 16; ++kk) {
+          const uint32_t aoff = (kk >> 2) * FA_TILE + (kk & 3) * 32;
+          tc_mma_f16(tdV, umma_desc_sw128(pt + aoff, 16, 1024),
+                     umma_desc_sw128(dob + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
+          tc_mma_f16(tdK, umma_desc_sw128(ds + aoff, 16, 1024),
+                     umma_desc_sw128(qb + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
+        }
+        if (j > 0) mbar_wait(dq_free, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < FA_BN / 16; ++kk)
+          tc_mma_f16(tdQ, umma_desc_sw128(ds + kk * 2048, FA_TILE, 1024),
+                     umma_desc_sw128(k_base + kk * 2048, 8192, 1024), id_dq, kk > 0);
+        tc_commit(dq_full);
+        tc_commit(&pbuf_free[bj]);
+        tc_commit(&q_empty[bj]);
+      };
       mbar_wait(kv_full, 0);
       for (int i = 0; i < n_q; ++i) {
         const int st = i & 1;
         mbar_wait(&q_full[st], (i >> 1) & 1);
-        if (i > 0) mbar_wait(ps_full, (i - 1) & 1);   // S^T / dP^T TMEM consumed
+        if (i > 0) mbar_wait(ps_full, (i - 1) & 1);   // S^T/dP^T(i-1) read, P^T/dS^T(i-1) written
         tc_fence_after();
         const uint32_t q_base = smem_u32(sQ + st * FA_TILE);
         const uint32_t do_base = smem_u32(sdO + st * FA_TILE);
@@ -447,31 +478,15 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
                      umma_desc_sw128(do_base + kk * 32, 16, 1024), id_st, kk > 0);
         }
         tc_commit(st_full);
-        mbar_wait(ps_full, i & 1);
-        tc_fence_after();
-        // dV += P^T dO ; dK += dS^T Q   (K = 128 queries: 2 chunks x 4 steps)
-#pragma unroll
-        for (int kk = 0; kk < FA_BM / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * FA_TILE + (kk & 3) * 32;
-          tc_mma_f16(tdV, umma_desc_sw128(pt_base + aoff, 16, 1024),
-                     umma_desc_sw128(do_base + kk * 2048, 8192, 1024), id_acc, (i | kk) != 0);
-          tc_mma_f16(tdK, umma_desc_sw128(dst_base + aoff, 16, 1024),
-                     umma_desc_sw128(q_base + kk * 2048, 8192, 1024), id_acc, (i | kk) != 0);
-        }
-        // dQ_i = dS K   (M = 128 queries from dS^T as MN-major A, K = 128 keys)
-        if (i > 0) mbar_wait(dq_free, (i - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < FA_BN / 16; ++kk)
-          tc_mma_f16(tdQ, umma_desc_sw128(dst_base + kk * 2048, FA_TILE, 1024),
-                     umma_desc_sw128(k_base + kk * 2048, 8192, 1024), id_dq, kk > 0);
-        tc_commit(dq_full);
-        tc_commit(mma_done);
-        tc_commit(&q_empty[st]);
+        if (i > 0) issue_acc(i - 1);
       }
+      mbar_wait(ps_full, (n_q - 1) & 1);
+      tc_fence_after();
+      issue_acc(n_q - 1);
+      tc_commit(acc_done);
     }
-  } else {
-    // 8 compute warps: lane quarter q = warp % 4 selects the TMEM lanes (key rows),
+  } else if (warp < 10) {
+    // 8 P/dS warps: lane quarter q = warp % 4 selects the TMEM lanes (key rows),
     // `half` selects which 64 of the 128 query columns this warp processes.
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -479,13 +494,15 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float sl2 = p.scale * 1.4426950408889634f;
     for (int i = 0; i < n_q; ++i) {
-      const int st = i & 1;
-      mbar_wait(&q_full[st], (i >> 1) & 1);   // lse / D of tile i visible
+      const int bi = i & 1;
+      mbar_wait(&q_full[bi], (i >> 1) & 1);   // lse / D of tile i staged
       mbar_wait(st_full, i & 1);
       tc_fence_after();
-      // P^T / dS^T smem is free once the MMAs of tile i-1 completed
-      if (i > 0) mbar_wait(mma_done, (i - 1) & 1);
-      const uint32_t lse_a = smem_u32(sLse + st * 128), d_a = smem_u32(sD + st * 128);
+      // this P^T / dS^T buffer was last read by the MMAs of tile i-2
+      if (i >= 2) mbar_wait(&pbuf_free[bi], ((i >> 1) & 1) ^ 1);
+      uint8_t* pt = sPt + bi * 2 * FA_TILE;
+      uint8_t* dst = sdSt + bi * 2 * FA_TILE;
+      const uint32_t lse_a = smem_u32(sLse + bi * 128), d_a = smem_u32(sD + bi * 128);
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {          // 16 queries per chunk
         const int c = half * 4 + cc;
@@ -496,9 +513,9 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float4 a = lds128(lse_a + (c * 16 + k * 4) * 4);
-          const float4 b = lds128(d_a + (c * 16 + k * 4) * 4);
+          const float4 bq = lds128(d_a + (c * 16 + k * 4) * 4);
           lse2[4 * k] = a.x; lse2[4 * k + 1] = a.y; lse2[4 * k + 2] = a.z; lse2[4 * k + 3] = a.w;
-          dvv[4 * k] = b.x; dvv[4 * k + 1] = b.y; dvv[4 * k + 2] = b.z; dvv[4 * k + 3] = b.w;
+          dvv[4 * k] = bq.x; dvv[4 * k + 1] = bq.y; dvv[4 * k + 2] = bq.z; dvv[4 * k + 3] = bq.w;
         }
         tmem_ld_wait();
         float pv[16], ds[16];
@@ -508,16 +525,16 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
           ds[e] = pv[e] * (__uint_as_float(d16[e]) - dvv[e]) * p.scale;
         }
         const int ch = c >> 2, u0 = (c & 3) * 2;
-        st_sw128(sPt + ch * FA_TILE, r, u0,
+        st_sw128(pt + ch * FA_TILE, r, u0,
                  make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]), pack_bf2(pv[4], pv[5]),
                             pack_bf2(pv[6], pv[7])));
-        st_sw128(sPt + ch * FA_TILE, r, u0 + 1,
+        st_sw128(pt + ch * FA_TILE, r, u0 + 1,
                  make_uint4(pack_bf2(pv[8], pv[9]), pack_bf2(pv[10], pv[11]),
                             pack_bf2(pv[12], pv[13]), pack_bf2(pv[14], pv[15])));
-        st_sw128(sdSt + ch * FA_TILE, r, u0,
+        st_sw128(dst + ch * FA_TILE, r, u0,
                  make_uint4(pack_bf2(ds[0], ds[1]), pack_bf2(ds[2], ds[3]), pack_bf2(ds[4], ds[5]),
                             pack_bf2(ds[6], ds[7])));
-        st_sw128(sdSt + ch * FA_TILE, r, u0 + 1,
+        st_sw128(dst + ch * FA_TILE, r, u0 + 1,
                  make_uint4(pack_bf2(ds[8], ds[9]), pack_bf2(ds[10], ds[11]),
                             pack_bf2(ds[12], ds[13]), pack_bf2(ds[14], ds[15])));
       }
@@ -525,28 +542,9 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ps_full);
-      // dQ_i: this thread owns query row r of tile i, columns [half*32, half*32+32)
-      mbar_wait(dq_full, i & 1);
-      tc_fence_after();
-      float* dq = p.dQacc + (int64_t)(row0 + i * FA_BM + r) * p.ld + hh * FA_D + half * 32;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t t16[16];
-        tmem_ld16(tdQ + lane_off + half * 32 + c * 16, t16);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 16; e += 4)
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 16 + e),
-                       "f"(__uint_as_float(t16[e])), "f"(__uint_as_float(t16[e + 1])),
-                       "f"(__uint_as_float(t16[e + 2])), "f"(__uint_as_float(t16[e + 3]))
-                       : "memory");
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_free);
     }
     // dK (half 0) / dV (half 1) epilogue: key row r
-    mbar_wait(mma_done, (n_q - 1) & 1);
+    mbar_wait(acc_done, 0);
     tc_fence_after();
     const int64_t grow = row0 + kt * FA_BN + r;
     const uint32_t tacc = half ? tdV : tdK;
@@ -556,15 +554,44 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       uint32_t t16[16];
       tmem_ld16(tacc + lane_off + c * 16, t16);
       tmem_ld_wait();
-      uint4* dst = reinterpret_cast<uint4*>(out + c * 16);
-      dst[0] = make_uint4(pack_bf2(__uint_as_float(t16[0]), __uint_as_float(t16[1])),
-                          pack_bf2(__uint_as_float(t16[2]), __uint_as_float(t16[3])),
-                          pack_bf2(__uint_as_float(t16[4]), __uint_as_float(t16[5])),
-                          pack_bf2(__uint_as_float(t16[6]), __uint_as_float(t16[7])));
-      dst[1] = make_uint4(pack_bf2(__uint_as_float(t16[8]), __uint_as_float(t16[9])),
-                          pack_bf2(__uint_as_float(t16[10]), __uint_as_float(t16[11])),
-                          pack_bf2(__uint_as_float(t16[12]), __uint_as_float(t16[13])),
-                          pack_bf2(__uint_as_float(t16[14]), __uint_as_float(t16[15])));
+      uint4* dstg = reinterpret_cast<uint4*>(out + c * 16);
+      dstg[0] = make_uint4(pack_bf2(__uint_as_float(t16[0]), __uint_as_float(t16[1])),
+                           pack_bf2(__uint_as_float(t16[2]), __uint_as_float(t16[3])),
+                           pack_bf2(__uint_as_float(t16[4]), __uint_as_float(t16[5])),
+                           pack_bf2(__uint_as_float(t16[6]), __uint_as_float(t16[7])));
+      dstg[1] = make_uint4(pack_bf2(__uint_as_float(t16[8]), __uint_as_float(t16[9])),
+                           pack_bf2(__uint_as_float(t16[10]), __uint_as_float(t16[11])),
+                           pack_bf2(__uint_as_float(t16[12]), __uint_as_float(t16[13])),
+                           pack_bf2(__uint_as_float(t16[14]), __uint_as_float(t16[15])));
+    }
+  } else {
+    // 4 dQ warps: query row r of tile i, fp32 reduction into dQacc
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    for (int i = 0; i < n_q; ++i) {
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      float* dq = p.dQacc + (int64_t)(row0 + i * FA_BM + r) * p.ld + hh * FA_D;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t t16[16];
+        tmem_ld16(tdQ + lane_off + c * 16, t16);
+        tmem_ld_wait();
+        if (c == 3) {   // dQ TMEM fully read: the next dQ MMA may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_free);
+        }
+#ifndef MP_FA_NO_DQ_RED
+#pragma unroll
+        for (int e = 0; e < 16; e += 4)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 16 + e),
+                       "f"(__uint_as_float(t16[e])), "f"(__uint_as_float(t16[e + 1])),
+                       "f"(__uint_as_float(t16[e + 2])), "f"(__uint_as_float(t16[e + 3]))
+                       : "memory");
+#endif
+      }
     }
   }
 
@@ -697,7 +724,12 @@ extern "C" int mp_attn_bwd(const void* q, const void* k, const void* v, const vo
     cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_BWD_SMEM);
     configured = true;
   }
-  FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, scale, lse, dvec, dq_acc,
+  static int* d_status = nullptr;
+  if (!d_status) {
+    cudaMalloc(&d_status, sizeof(int));
+    cudaMemset(d_status, 0, sizeof(int));
+  }
+  FaBwdParams p{d_status, (int)B, (int)H, (int)s, (int)ld, scale, lse, dvec, dq_acc,
                 reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
   dim3 grid((unsigned)(s / FA_BN), (unsigned)(B * H));
   fa_bwd_kernel<<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, p);

@@ -36,6 +36,8 @@ struct GemmParams {
   int epi;            // 0 none, 1 gelu, 2 +aux, 3 *gelu'(aux), 4 C=pre & aux:=gelu(pre)
   uint16_t* aux;      // bf16 (M x N) with row stride aux_ld (input for 2/3, output for 4)
   int64_t aux_ld, aux_bs0, aux_bs1;
+  int n_wide;         // 2-CTA kernel: tiles [0, n_wide) are 256 x BN; the rest are
+                      // half-width splits of the last partial wave (wave-quantisation fix)
 };
 
 template <int BN>
@@ -372,10 +374,33 @@ __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
       : "memory");
 }
 
+struct Tile2 {
+  int b0, b1, mb, n0;
+  bool narrow;
+};
+template <int BN>
+__device__ __forceinline__ Tile2 decode2(const GemmParams& p, int t) {
+  const int tiles_mn = p.tiles_m * p.tiles_n;
+  int w = t, extra = 0;
+  bool narrow = false;
+  if (t >= p.n_wide) {
+    const int u = t - p.n_wide;
+    w = p.n_wide + (u >> 1);
+    extra = (u & 1) * (BN / 2);
+    narrow = true;
+  }
+  const int b = w / tiles_mn;
+  const int rem = w - b * tiles_mn;
+  const int mb = rem / p.tiles_n;
+  const int nb = rem - mb * p.tiles_n;
+  return Tile2{b / p.nb1, b - (b / p.nb1) * p.nb1, mb, nb * BN + extra, narrow};
+}
+
 template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
-                         const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+                         const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmBn, const GemmParams p) {
   using Cfg = Gemm2Cfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -419,24 +444,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int tiles_mn = p.tiles_m * p.tiles_n;   // tiles_m counts 256-row pair tiles
-
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < p.num_tiles; t += npairs) {
-        const int b = t / tiles_mn;
-        const int rem = t - b * tiles_mn;
-        const int mb = rem / p.tiles_n;
-        const int nb = rem - mb * p.tiles_n;
-        const int b0 = b / p.nb1, b1 = b - (b / p.nb1) * p.nb1;
-        const int m0 = mb * 2 * BM + rank * BM;
-        const int n0 = nb * BN + rank * (BN / 2);
+        const Tile2 tl = decode2<BN>(p, t);
+        const int b0 = tl.b0, b1 = tl.b1;
+        const int m0 = tl.mb * 2 * BM + rank * BM;
+        const int nw = tl.narrow ? BN / 4 : BN / 2;       // B columns staged by this CTA
+        const int n0 = tl.n0 + rank * nw;
+        const uint32_t bytes = 2u * (Cfg::A_BYTES + nw * BK * 2);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
           uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
           uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
           const int k0 = kb * BK;
@@ -448,11 +470,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_4d_2sm(&tmA, fb, a_dst, k0, m0, b1, b0);
           }
           if (p.b_mn) {
-#pragma unroll
-            for (int i = 0; i < BN / 128; ++i)
+            for (int i = 0; i < nw / 64; ++i)
               tma_load_4d_2sm(&tmB, fb, b_dst + i * 8192, n0 + 64 * i, k0, b1, b0);
           } else {
-            tma_load_4d_2sm(&tmB, fb, b_dst, k0, n0, b1, b0);
+            tma_load_4d_2sm(tl.narrow ? &tmBn : &tmB, fb, b_dst, k0, n0, b1, b0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -463,7 +484,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      const uint32_t idesc = umma_idesc_bf16(2 * BM, BN, p.a_mn, p.b_mn);
+      const uint32_t idesc_w = umma_idesc_bf16(2 * BM, BN, p.a_mn, p.b_mn);
+      const uint32_t idesc_n = umma_idesc_bf16(2 * BM, BN / 2, p.a_mn, p.b_mn);
       const uint32_t a_lbo = p.a_mn ? 8192u : 16u, b_lbo = p.b_mn ? 8192u : 16u;
       const uint32_t a_kstep = p.a_mn ? 2048u : 32u, b_kstep = p.b_mn ? 2048u : 32u;
       int stage = 0;
@@ -471,6 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = pair; t < p.num_tiles; t += npairs) {
+        const uint32_t idesc = (t >= p.n_wide) ? idesc_n : idesc_w;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -505,21 +528,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = pair; t < p.num_tiles; t += npairs) {
-      const int b = t / tiles_mn;
-      const int rem = t - b * tiles_mn;
-      const int mb = rem / p.tiles_n;
-      const int nb = rem - mb * p.tiles_n;
-      const int b0 = b / p.nb1, b1 = b - (b / p.nb1) * p.nb1;
+      const Tile2 tl = decode2<BN>(p, t);
+      const int b0 = tl.b0, b1 = tl.b1;
       const int64_t row_off = (int64_t)b0 * p.c_bs0 + (int64_t)b1 * p.c_bs1;
-      const int m = mb * 2 * BM + rank * BM + row;
+      const int m = tl.mb * 2 * BM + rank * BM + row;
+      const int width = tl.narrow ? BN / 2 : BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+      for (int c = half * (width / 64); c < (half + 1) * (width / 64); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
-        const int n = nb * BN + c * 32;
+        const int n = tl.n0 + c * 32;
         if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r, b0, b1);
       }
       tc_fence_before();
@@ -616,8 +637,8 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams 
 
 
 template <int BN>
-static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams p,
-                           cudaStream_t stream) {
+static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbn,
+                           GemmParams p, cudaStream_t stream) {
   using Cfg = Gemm2Cfg<BN>;
   static bool configured = false;
   if (!configured) {
@@ -631,10 +652,17 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, GemmPar
   }
   p.tiles_m = (p.M + 2 * BM - 1) / (2 * BM);
   p.tiles_n = (p.N + BN - 1) / BN;
-  p.num_tiles = p.tiles_m * p.tiles_n * p.nb0 * p.nb1;
+  const int wide = p.tiles_m * p.tiles_n * p.nb0 * p.nb1;
   int pairs = num_sms() / 2;
+  // Wave quantisation: when the last wave is less than half full, split its
+  // tiles into two half-width tiles so it finishes in half the time.
+  static const bool no_split = getenv("MPEXEC_GEMM_NO_TAIL_SPLIT") != nullptr;
+  const int r = wide % pairs;
+  p.n_wide = wide;
+  if (!no_split && BN == 256 && wide > pairs && r > 0 && 2 * r <= pairs) p.n_wide = wide - r;
+  p.num_tiles = p.n_wide + 2 * (wide - p.n_wide);
   if (p.num_tiles < pairs) pairs = p.num_tiles;
-  gemm_bf16_2sm_kernel<BN><<<2 * pairs, kThreads, Cfg::SMEM, stream>>>(ma, mb, p);
+  gemm_bf16_2sm_kernel<BN><<<2 * pairs, kThreads, Cfg::SMEM, stream>>>(ma, mb, mbn, p);
   return 0;
 }
 
@@ -733,12 +761,18 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
     BN = (N > 128) ? 256 : (N > 64 ? 128 : 64);
   }
   const int b_box_n = two_sm ? BN / 2 : BN;
+  CUtensorMap mbn;
   if (bd[3] == 1) {
     p.b_mn = 1;
     rc = make_map(&mb, B, N, K, bd[2], nbatch1, bd[5], nbatch0, bd[4], 64, BK);
+    mbn = mb;
   } else if (bd[2] == 1) {
     p.b_mn = 0;
     rc = make_map(&mb, B, K, N, bd[3], nbatch1, bd[5], nbatch0, bd[4], BK, b_box_n);
+    if (!rc && two_sm)
+      rc = make_map(&mbn, B, K, N, bd[3], nbatch1, bd[5], nbatch0, bd[4], BK, b_box_n / 2);
+    else
+      mbn = mb;
   } else {
     set_error("mp_gemm_bf16: B needs a unit stride");
     return 2;
@@ -747,7 +781,8 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (two_sm)
-    rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, p, s) : launch_gemm_2sm<128>(ma, mb, p, s);
+    rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, mbn, p, s)
+                     : launch_gemm_2sm<128>(ma, mb, mbn, p, s);
   else if (BN == 256)
     rc = launch_gemm<256>(ma, mb, p, s);
   else if (BN == 128)

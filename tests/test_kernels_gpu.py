@@ -28,7 +28,8 @@ def _seed():
 
 
 GEMM_SHAPES = [(128, 256, 64), (256, 512, 128), (384, 256, 1024), (64, 1024, 1024),
-               (1000, 520, 136), (512, 64, 512), (256, 128, 192), (2048, 2048, 2048)]
+               (1000, 520, 136), (512, 64, 512), (256, 128, 192), (2048, 2048, 2048),
+               (8192, 2048, 128), (6144, 4096, 64)]   # last two: tail-wave split
 
 
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
