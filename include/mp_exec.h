@@ -136,6 +136,22 @@ int mp_unpack_box(const void* src, void* dst, const int64_t* dst_strides,
                   const int64_t* lo, const int64_t* ext, int rank, int elem_bytes,
                   void* stream);
 
+/* ---- NCCL communicators (owned by the library, driven on the caller's stream,
+ * capturable in CUDA graphs).  Replace the modeled collective_time /
+ * transfer_time of the reference (costs.py:63-92).  dtype: 0 bf16, 1 fp32,
+ * 2 bytes.  op: 0 sum, 1 max.  Peers are ranks within the communicator. */
+int mp_nccl_version(void);
+int mp_nccl_unique_id(void* out128);
+int mp_comm_init(const void* uid128, int nranks, int rank, void** comm_out);
+int mp_comm_destroy(void* comm);
+int mp_allreduce(void* comm, void* buf, int64_t count, int dtype, int op, void* stream);
+int mp_allgather(void* comm, const void* send, void* recv, int64_t sendcount, int dtype,
+                 void* stream);
+int mp_group_start(void);
+int mp_group_end(void);
+int mp_send(void* comm, const void* buf, int64_t count, int dtype, int peer, void* stream);
+int mp_recv(void* comm, void* buf, int64_t count, int dtype, int peer, void* stream);
+
 /* ---- optimizer (weight update after the ZeRO rewrite, intra.py:404-424) ---
  * Fused Adam over flat fp32 master/m/v/grad buffers, writing the bf16
  * working copy; grad is scaled by grad_scale before use. */

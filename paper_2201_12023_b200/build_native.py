@@ -14,14 +14,30 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmpexec.so"
-SOURCES = ["gemm_sm100.cu", "attention.cu", "ops.cu"]
+SOURCES = ["gemm_sm100.cu", "attention.cu", "ops.cu", "comm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir() -> Path:
+    """The NCCL torch ships (the one already loaded in-process when the library
+    is used), so both sides agree on one libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = Path(base) / "nccl"
+        if (d / "include" / "nccl.h").exists():
+            return d
+    return Path("/usr")
+
+
+NCCL = _nccl_dir()
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
     "-Xptxas", "-v",
     "-I", str(PKG.parent / "include"),
+    "-I", str(NCCL / "include"),
 ]
 
 
@@ -36,7 +52,9 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(LIB) + ".tmp", "-lcuda"]
+    nccl_lib = NCCL / "lib"
+    cmd = [NVCC, *FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(LIB) + ".tmp",
+           "-L", str(nccl_lib), "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}", "-lcuda"]
     # libcuda is resolved at run time through cudaGetDriverEntryPoint; link the stub
     # only so the symbol table is complete when a driver is absent (CPU container).
     stub = Path("/usr/local/cuda/lib64/stubs")

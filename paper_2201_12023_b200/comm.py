@@ -1,27 +1,43 @@
-"""Communicators for one rank: NCCL over NVLink/NVSwitch through torch.distributed
-(plumbing only; payloads are packed/unpacked by libmpexec kernels).
+"""Communicators for one rank: NCCL communicators owned by libmpexec (mp_comm_*)
+and driven on the caller's CUDA stream — no torch.distributed call on the hot
+path (torch's process groups only bootstrap the unique ids and run step-level
+barriers / scalar reductions).
 
-Groups are derived from the plan and created identically on every rank (the
-torch.distributed rule for new_group):
+Groups are derived from the plan and created identically on every rank:
   * per stage, per axis set {0}, {1}, {0,1}: the devices that differ from a
     device only along those axes (LogicalMesh.coord_device, mesh.py:111-114) —
     the k-group of an all_reduce (sharding.py:284-291) and the softmax row group;
   * per stage: all its devices (generic intra-mesh relayout P2P);
   * per cross-mesh boundary (reshard.py:276-328): the union of both stages'
-    devices — one communicator per direction, so forward activations and
-    backward gradients between the same stage pair never serialise on one
-    NCCL stream (a 1F1B deadlock otherwise);
+    devices — one communicator per direction; the sender drives it on its send
+    stream and the receiver on its compute stream, so forward activations and
+    backward gradients between a stage pair never queue behind each other
+    (with one stream, 1F1B deadlocks: stage i's blocked send of f_{b+1}
+    precedes its recv of b_b);
   * per GatherOp replica group (reshard.py:155-156): the local all-gather.
+Group ranks are ordered by global device id (= NCCL rank order).
 """
 from __future__ import annotations
 
-from typing import Optional
+from dataclasses import dataclass, field
 
 import torch
 import torch.distributed as dist
 
+from . import native
 from .plan import ExecPlan, Mesh
 from .schedule import Program
+
+
+@dataclass
+class Group:
+    key: tuple
+    ranks: tuple[int, ...]
+    comm: int = 0
+    local: dict = field(default_factory=dict)
+
+    def peer(self, global_rank: int) -> int:
+        return self.local[global_rank]
 
 
 class Comm:
@@ -29,7 +45,7 @@ class Comm:
         self.rank = rank
         self.world = world
         self.enabled = world > 1
-        self._groups: dict[tuple, object] = {}
+        self._groups: dict[tuple, Group] = {}
         if not self.enabled:
             return
         if not dist.is_initialized():
@@ -55,40 +71,60 @@ class Comm:
             for bt in bd.tensors:
                 for g in bt.xplan.gathers:
                     keys.append(("gather", bd.producer, bd.consumer, g.devices))
+        uniq = []
         for k in keys:
-            if k in self._groups:
-                continue
-            ranks = list(k[-1])
-            # always a fresh communicator (never WORLD): directions must not share a stream
-            self._groups[k] = dist.new_group(ranks=ranks)
-        # a private world group for step-level reductions (loss, barrier)
+            if k not in self._groups:
+                self._groups[k] = Group(k, tuple(k[-1]), 0,
+                                        {r: i for i, r in enumerate(k[-1])})
+                uniq.append(k)
+        # one round of unique-id exchange: each group's lowest rank makes its id
+        mine = {k: native.nccl_unique_id() for k in uniq if self._groups[k].ranks[0] == rank}
+        allids: list = [None] * world
+        dist.all_gather_object(allids, mine)
+        ids = {}
+        for part in allids:
+            ids.update(part)
+        # same global order on every rank -> no init deadlock
+        for k in uniq:
+            g = self._groups[k]
+            if rank in g.local:
+                g.comm = native.comm_init(ids[k], len(g.ranks), g.local[rank])
+        # torch group for step-level reductions (loss, barrier, max time)
         self.world_group = dist.new_group(ranks=list(range(world)))
 
-    def stage_group(self, st_index: int, mesh: Mesh):
+    def stage_group(self, st_index: int, mesh: Mesh) -> Group:
         return self._groups[("stage", st_index, tuple(sorted(mesh.device_ids)))]
 
-    def axis_group(self, st_index: int, mesh: Mesh, axes: tuple[int, ...], device: int):
+    def axis_group(self, st_index: int, mesh: Mesh, axes: tuple[int, ...], device: int) -> Group:
         return self._groups[("axis", st_index, axes, mesh.axis_group(device, axes))]
 
-    def boundary_group(self, bd, plan: ExecPlan):
+    def boundary_group(self, bd, plan: ExecPlan) -> Group:
         ranks = tuple(sorted(set(plan.stages[bd.producer].mesh.device_ids)
                              | set(plan.stages[bd.consumer].mesh.device_ids)))
         return self._groups[("boundary", bd.producer, bd.consumer, ranks)]
 
-    def gather_group(self, bd, devices: tuple[int, ...]):
+    def gather_group(self, bd, devices: tuple[int, ...]) -> Group:
         return self._groups[("gather", bd.producer, bd.consumer, devices)]
 
     # ------------------------------------------------------------------ ops
-    def all_reduce(self, t: torch.Tensor, group, op=dist.ReduceOp.SUM) -> None:
-        dist.all_reduce(t, op=op, group=group)
+    # All ops are enqueued on the current CUDA stream (or `stream`).
+    def all_reduce(self, t: torch.Tensor, group: Group, op=dist.ReduceOp.SUM, stream=None) -> None:
+        native.allreduce(group.comm, t, 1 if op == dist.ReduceOp.MAX else 0, stream)
 
-    def p2p(self, sends: list[tuple[torch.Tensor, int]], recvs: list[tuple[torch.Tensor, int]],
-            group) -> list:
-        ops = [dist.P2POp(dist.isend, t, peer, group=group) for t, peer in sends]
-        ops += [dist.P2POp(dist.irecv, t, peer, group=group) for t, peer in recvs]
-        if not ops:
+    def p2p(self, sends, recvs, group: Group, stream=None) -> list:
+        """sends / recvs: [(tensor, global peer rank)] in one NCCL group."""
+        if not sends and not recvs:
             return []
-        return dist.batch_isend_irecv(ops)
+        native.send_recv(group.comm, [(t, group.peer(p)) for t, p in sends],
+                         [(t, group.peer(p)) for t, p in recvs], stream)
+        return []
 
-    def all_gather_into(self, out_flat: torch.Tensor, in_flat: torch.Tensor, group) -> None:
-        dist.all_gather_into_tensor(out_flat, in_flat, group=group)
+    def all_gather_into(self, out_flat: torch.Tensor, in_flat: torch.Tensor, group: Group,
+                        stream=None) -> None:
+        native.allgather(group.comm, out_flat, in_flat, stream)
+
+    def close(self) -> None:
+        for g in self._groups.values():
+            if g.comm:
+                native.comm_destroy(g.comm)
+                g.comm = 0

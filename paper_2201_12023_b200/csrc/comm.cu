@@ -1,0 +1,125 @@
+// NCCL communicators of the plan executor, owned by the C side and driven on
+// the caller's CUDA stream (so they can sit inside CUDA-graph captures and carry
+// no per-call Python overhead).  Replaces the modeled `collective_time` /
+// `transfer_time` of the reference (costs.py:63-92) for:
+//   all_reduce   k-split matmul partial sums (sharding.py:284-291), split-softmax
+//                row statistics, gradient reduction (intra.py:404-424)
+//   all_gather   local all-gather of a cross-mesh replica group (reshard.py:155)
+//                and dim-0 relayouts
+//   send / recv  cross-mesh Transfers (reshard.py:32-37) and box relayouts
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <string>
+#include "common.cuh"
+#include "../../include/mp_exec.h"
+
+namespace mp {
+
+static ncclDataType_t nccl_dtype(int d) {
+  switch (d) {
+    case 0: return ncclBfloat16;
+    case 1: return ncclFloat32;
+    default: return ncclUint8;
+  }
+}
+
+#define MP_NCCL(call)                                                                  \
+  do {                                                                                 \
+    ncclResult_t r__ = (call);                                                         \
+    if (r__ != ncclSuccess) {                                                          \
+      ::mp::set_error(std::string(__func__) + ": " + ncclGetErrorString(r__) + " (" +  \
+                      ncclGetLastError(nullptr) + ")");                                \
+      return 1;                                                                        \
+    }                                                                                  \
+  } while (0)
+
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" {
+
+int mp_nccl_version(void) {
+  int v = 0;
+  ncclGetVersion(&v);
+  return v;
+}
+
+int mp_nccl_unique_id(void* out128) {
+  clear_error();
+  MP_CHECK_ARG(out128, "null output");
+  ncclUniqueId id;
+  MP_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "unexpected ncclUniqueId size");
+  memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+int mp_comm_init(const void* uid128, int nranks, int rank, void** comm_out) {
+  clear_error();
+  MP_CHECK_ARG(uid128 && comm_out && nranks >= 1 && rank >= 0 && rank < nranks, "bad args");
+  ncclUniqueId id;
+  memcpy(&id, uid128, sizeof(id));
+  ncclComm_t c;
+  MP_NCCL(ncclCommInitRank(&c, nranks, id, rank));
+  *comm_out = c;
+  return 0;
+}
+
+int mp_comm_destroy(void* comm) {
+  clear_error();
+  if (!comm) return 0;
+  MP_NCCL(ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm)));
+  return 0;
+}
+
+int mp_allreduce(void* comm, void* buf, int64_t count, int dtype, int op, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(comm && buf && count >= 0 && (op == 0 || op == 1), "bad args");
+  if (count == 0) return 0;
+  MP_NCCL(ncclAllReduce(buf, buf, (size_t)count, nccl_dtype(dtype), op ? ncclMax : ncclSum,
+                        reinterpret_cast<ncclComm_t>(comm), reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int mp_allgather(void* comm, const void* send, void* recv, int64_t sendcount, int dtype,
+                 void* stream) {
+  clear_error();
+  MP_CHECK_ARG(comm && send && recv && sendcount >= 0, "bad args");
+  if (sendcount == 0) return 0;
+  MP_NCCL(ncclAllGather(send, recv, (size_t)sendcount, nccl_dtype(dtype),
+                        reinterpret_cast<ncclComm_t>(comm), reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int mp_group_start(void) {
+  clear_error();
+  MP_NCCL(ncclGroupStart());
+  return 0;
+}
+
+int mp_group_end(void) {
+  clear_error();
+  MP_NCCL(ncclGroupEnd());
+  return 0;
+}
+
+int mp_send(void* comm, const void* buf, int64_t count, int dtype, int peer, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(comm && buf && count >= 0 && peer >= 0, "bad args");
+  if (count == 0) return 0;
+  MP_NCCL(ncclSend(buf, (size_t)count, nccl_dtype(dtype), peer,
+                   reinterpret_cast<ncclComm_t>(comm), reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int mp_recv(void* comm, void* buf, int64_t count, int dtype, int peer, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(comm && buf && count >= 0 && peer >= 0, "bad args");
+  if (count == 0) return 0;
+  MP_NCCL(ncclRecv(buf, (size_t)count, nccl_dtype(dtype), peer,
+                   reinterpret_cast<ncclComm_t>(comm), reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+}  // extern "C"

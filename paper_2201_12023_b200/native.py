@@ -46,6 +46,16 @@ EXPORTS = {
                      c_vp], c_int),
     "mp_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
                      c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
+    "mp_nccl_version": ([], c_int),
+    "mp_nccl_unique_id": ([c_vp], c_int),
+    "mp_comm_init": ([c_vp, c_int, c_int, ctypes.POINTER(c_vp)], c_int),
+    "mp_comm_destroy": ([c_vp], c_int),
+    "mp_allreduce": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
+    "mp_allgather": ([c_vp, c_vp, c_vp, c_i64, c_int, c_vp], c_int),
+    "mp_group_start": ([], c_int),
+    "mp_group_end": ([], c_int),
+    "mp_send": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
+    "mp_recv": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
     "mp_pack_box": ([c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp, c_vp], c_int),
     "mp_unpack_box": ([c_vp, c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp], c_int),
     "mp_adam_step": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_f32, c_f32, c_f32, c_f32, c_f32,
@@ -419,3 +429,56 @@ def accum_bf16_f32(x: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Ten
     _check(load().mp_accum_bf16_f32(x.data_ptr(), out.data_ptr(), x.numel(), _stream(stream)),
            "mp_accum_bf16_f32")
     return out
+
+
+# --------------------------------------------------------------------------- NCCL
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return 0
+    if t.dtype == torch.float32:
+        return 1
+    raise NativeError(f"unsupported collective dtype {t.dtype}")
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().mp_nccl_unique_id(buf), "mp_nccl_unique_id")
+    return buf.raw
+
+
+def comm_init(uid: bytes, nranks: int, rank: int) -> int:
+    out = c_vp()
+    _check(load().mp_comm_init(ctypes.create_string_buffer(uid, 128), nranks, rank,
+                               ctypes.byref(out)), "mp_comm_init")
+    return out.value
+
+
+def comm_destroy(comm: int) -> None:
+    _check(load().mp_comm_destroy(comm), "mp_comm_destroy")
+
+
+def allreduce(comm: int, t: torch.Tensor, op: int = 0, stream=None) -> None:
+    if not t.is_contiguous():
+        raise NativeError("allreduce needs a contiguous tensor")
+    _check(load().mp_allreduce(comm, t.data_ptr(), t.numel(), _dt(t), op, _stream(stream)),
+           "mp_allreduce")
+
+
+def allgather(comm: int, out: torch.Tensor, inp: torch.Tensor, stream=None) -> None:
+    _check(load().mp_allgather(comm, inp.data_ptr(), out.data_ptr(), inp.numel(), _dt(inp),
+                               _stream(stream)), "mp_allgather")
+
+
+def send_recv(comm: int, sends, recvs, stream=None) -> None:
+    """One NCCL group of sends [(tensor, peer)] and recvs [(tensor, peer)]."""
+    lib = load()
+    st = _stream(stream)
+    _check(lib.mp_group_start(), "mp_group_start")
+    try:
+        for t, peer in sends:
+            _check(lib.mp_send(comm, t.data_ptr(), t.numel(), _dt(t), peer, st), "mp_send")
+        for t, peer in recvs:
+            _check(lib.mp_recv(comm, t.data_ptr(), t.numel(), _dt(t), peer, st), "mp_recv")
+    finally:
+        _check(lib.mp_group_end(), "mp_group_end")

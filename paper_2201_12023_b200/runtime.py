@@ -147,7 +147,8 @@ class StageRunner:
         self.keep_outputs = False
         self._host_input_bufs: dict = {}
         self.h2d_bytes = 0
-        self.pending_sends: list = []
+        self.send_stream = torch.cuda.Stream()
+        self.sends_pending = False
         self.input_mode = "host" if host_inputs else ("fn" if inputs is not None else "resident")
         self._resident_inputs: dict = {}
 
@@ -842,6 +843,8 @@ class StageRunner:
                 w.wait()
 
     def send(self, ins: Instr):
+        """Cross-mesh sends run on a dedicated stream (after the compute that
+        produced them) so a blocked send never stalls this stage's receives."""
         bd = ins.boundary
         mb = ins.microbatch
         sends = []
@@ -854,7 +857,12 @@ class StageRunner:
             view = native.box_view(v, lo, ext)
             sends.append((view if view is not None else native.pack_box(v, lo, ext), t.dst_device))
         if sends:
-            self.pending_sends += self.comm.p2p(sends, [], self.comm.boundary_group(bd, self.plan))
+            self.send_stream.wait_stream(torch.cuda.current_stream())
+            self.comm.p2p(sends, [], self.comm.boundary_group(bd, self.plan),
+                          stream=self.send_stream)
+            for buf, _ in sends:
+                buf.record_stream(self.send_stream)
+            self.sends_pending = True
 
     def free(self, ins: Instr):
         if ins.buffer and ins.buffer.startswith("act"):
@@ -937,9 +945,9 @@ class StageRunner:
             elif ins.op == "free":
                 self.free(ins)
             elif ins.op == "sync":
-                for w in self.pending_sends:
-                    w.wait()
-                self.pending_sends = []
+                if self.sends_pending:
+                    torch.cuda.current_stream().wait_stream(self.send_stream)
+                    self.sends_pending = False
                 if update:
                     self.optimizer_step()
             if record and ins.op in ("compute", "send", "recv", "all_gather"):
