@@ -329,7 +329,6 @@ __global__ void __launch_bounds__(192, 2)
 
 // ------------------------------------------------------------------ backward
 struct FaBwdParams {
-  int* status;        // set to 1 if the kernel could not run (smem misaligned)
   int B, H, s, ld;
   float scale;        // 1/sqrt(d)
   const float* lse;   // [B*H, s]
@@ -352,8 +351,8 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                   const FaBwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  if (smem_u32(smem_raw) & 1023) {
-    if (threadIdx.x == 0) atomicExch(p.status, 1);
+  if (smem_u32(smem_raw) & 1023) {   // never observed; poison dQ so parity tests catch it
+    if (threadIdx.x == 0) p.dQacc[0] = __int_as_float(0x7fc00000);
     return;
   }
   uint8_t* smem = smem_raw;
@@ -724,12 +723,7 @@ extern "C" int mp_attn_bwd(const void* q, const void* k, const void* v, const vo
     cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_BWD_SMEM);
     configured = true;
   }
-  static int* d_status = nullptr;
-  if (!d_status) {
-    cudaMalloc(&d_status, sizeof(int));
-    cudaMemset(d_status, 0, sizeof(int));
-  }
-  FaBwdParams p{d_status, (int)B, (int)H, (int)s, (int)ld, scale, lse, dvec, dq_acc,
+  FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, scale, lse, dvec, dq_acc,
                 reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
   dim3 grid((unsigned)(s / FA_BN), (unsigned)(B * H));
   fa_bwd_kernel<<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, p);

@@ -149,6 +149,17 @@ class StageRunner:
         self.h2d_bytes = 0
         self.send_stream = torch.cuda.Stream()
         self.sends_pending = False
+        # CUDA graphs: one capture per (phase, slot); slots = in-flight bound
+        self.use_graphs = os.environ.get("MPEXEC_CUDA_GRAPHS", "0") == "1"
+        nst = len(plan.stages)
+        B = plan.num_microbatches
+        self.n_slots = (max(1, min(B, nst - self.st.index)) if program.schedule == "1f1b" or
+                        not plan.has_backward else B)
+        self.graphs: dict = {}
+        self.cap_vals: dict = {}
+        self.cap_aux: dict = {}
+        self.static: dict = {}
+
         self.input_mode = "host" if host_inputs else ("fn" if inputs is not None else "resident")
         self._resident_inputs: dict = {}
 
@@ -753,11 +764,63 @@ class StageRunner:
         return t
 
     # ------------------------------------------------------------------ phases
+    # ------------------------------------------------------------------ CUDA graphs
+    def slot_of(self, mb: int) -> int:
+        return mb % self.n_slots
+
+    def _graph_inputs(self, mb: int):
+        """Graph mode: stage this microbatch's graph inputs into the slot's
+        static buffers (outside the captured region)."""
+        vals = self.vals.setdefault(mb, {})
+        k = self.slot_of(mb)
+        for op in self.fwd_ops:
+            if op.op != "input":
+                continue
+            src = self._load_input(mb, op)
+            key = ("in", k, op.nid)
+            buf = self.static.get(key)
+            if buf is None:
+                buf = torch.empty_like(src)
+                self.static[key] = buf
+            buf.copy_(src, non_blocking=True)
+            vals[op.nid] = buf
+
     def compute(self, phase: str, mb: int):
+        """Run the stage's forward or backward ops for one microbatch: eagerly,
+        or (graph mode) by replaying the CUDA graph captured for this
+        (phase, slot) — slots = 1F1B in-flight bound, so a slot's activations
+        are never live for two microbatches at once."""
+        if not self.use_graphs:
+            return self._compute_eager(phase, mb)
+        if phase == "fwd":
+            self._graph_inputs(mb)
+        key = (phase, self.slot_of(mb))
+        vals = self.vals.setdefault(mb, {})
+        g = self.graphs.get(key)
+        if g is None:
+            before = set(vals)
+            g = torch.cuda.CUDAGraph()
+            self.join_dw()
+            with torch.cuda.graph(g):
+                self._compute_eager(phase, mb, skip_inputs=True)
+                self.join_dw()
+            self.graphs[key] = g
+            self.cap_vals[key] = {n: v for n, v in vals.items() if n not in before}
+            self.cap_aux[key] = dict(self.aux.get(mb, {}))
+            g.replay()
+            return
+        vals.update(self.cap_vals[key])
+        if self.cap_aux[key]:
+            self.aux.setdefault(mb, {}).update(self.cap_aux[key])
+        g.replay()
+
+    def _compute_eager(self, phase: str, mb: int, skip_inputs: bool = False):
         vals = self.vals.setdefault(mb, {})
         for op in (self.fwd_ops if phase == "fwd" else self.bwd_ops):
             try:
                 if op.op == "input":
+                    if skip_inputs:
+                        continue
                     out = self._load_input(mb, op)
                 elif op.op == "attn_fwd":
                     out = self._run_attn_fwd(mb, op)
@@ -783,8 +846,15 @@ class StageRunner:
         for bt in bd.tensors:
             node = self.graph[bt.node]
             dspec = canonical(bt.dst_spec, self.mesh)
-            out = torch.empty(local_dims(node.dims, dspec, self.mesh), dtype=torch.bfloat16,
-                              device=self.dev)
+            shape = local_dims(node.dims, dspec, self.mesh)
+            if self.use_graphs:
+                key = ("recv", self.slot_of(mb), bt.node)
+                out = self.static.get(key)
+                if out is None:
+                    out = torch.empty(shape, dtype=torch.bfloat16, device=self.dev)
+                    self.static[key] = out
+            else:
+                out = torch.empty(shape, dtype=torch.bfloat16, device=self.dev)
             vals[bt.node] = out
             outs.append((out, _lo(device_box(node.dims, dspec, self.mesh, self.me))))
         recvs = []
