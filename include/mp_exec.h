@@ -166,6 +166,15 @@ int mp_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream);
 /* y(fp32) += x(bf16)  (gradient accumulation of a bf16 partial). */
 int mp_accum_bf16_f32(const void* x, float* y, int64_t n, void* stream);
 
+/* ---- planner acceleration --------------------------------
+ * Exact branch-and-bound of the intra-op strategy ILP with the reference's
+ * semantics (intra.py:323-401: greedy incumbent, suffix bound, index-order DFS,
+ * strict improvement, node budget).  Host-only (no device work).  Costs are
+ * integers in one common unit (the caller scales the exact rationals). */
+int mp_ilp_solve(int n, const int* k, const int64_t* costs, int n_edges, const int* u,
+                 const int* v, const int64_t* mats, int64_t budget, int* choice_out,
+                 int64_t* objective_out, int* certified_out, int64_t* explored_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,6 +56,9 @@ EXPORTS = {
     "mp_group_end": ([], c_int),
     "mp_send": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
     "mp_recv": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
+    "mp_ilp_solve": ([c_int, ctypes.POINTER(c_int), c_i64p, c_int, ctypes.POINTER(c_int),
+                      ctypes.POINTER(c_int), c_i64p, c_i64, ctypes.POINTER(c_int), c_i64p,
+                      ctypes.POINTER(c_int), c_i64p], c_int),
     "mp_pack_box": ([c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp, c_vp], c_int),
     "mp_unpack_box": ([c_vp, c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp], c_int),
     "mp_adam_step": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_f32, c_f32, c_f32, c_f32, c_f32,

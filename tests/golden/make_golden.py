@@ -162,9 +162,29 @@ def make_programs():
                  {"plan": doc, "program": prog.to_json()})
 
 
+def make_ilp_tables():
+    """Random strategy tables (integer and rational costs, both edge
+    orientations, tight and default budgets) with the reference solver's answer."""
+    import sys as _sys
+    _sys.path.insert(0, str(HERE.parent))
+    from test_ilp_native import enc, rand_table
+    from meshplan.intra import solve_ilp
+    rng = random.Random(123)
+    out = []
+    for trial in range(48):
+        t = rand_table(rng, rng.randint(1, 12), 7, rational=trial % 2 == 1, flip=trial % 3 == 0)
+        budget = (3, 60, 200_000)[trial % 3]
+        r = solve_ilp(t, budget)
+        out.append({"table": enc(t), "budget": budget, "choice": list(r.choice),
+                    "objective": [r.objective.numerator, r.objective.denominator],
+                    "certified": bool(r.certified)})
+    return out
+
+
 if __name__ == "__main__":
     dump(HERE / "xmesh.json.gz", make_xmesh())
     dump(HERE / "boxes.json.gz", make_boxes())
     dump(HERE / "algorithms.json.gz", make_algorithms())
     make_programs()
+    dump(HERE / "ilp_tables.json.gz", make_ilp_tables())
     print("golden fixtures written to", HERE)
