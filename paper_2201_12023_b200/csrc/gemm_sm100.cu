@@ -73,7 +73,9 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off
               pack_bf2(gelu_tanh(v[8 * i + 4]), gelu_tanh(v[8 * i + 5])),
               pack_bf2(gelu_tanh(v[8 * i + 6]), gelu_tanh(v[8 * i + 7])));
       } else {
-        for (int i = 0; i < 32 && n + i < p.N; ++i) ax[i] = f2bf(gelu_tanh(v[i]));
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (n + i < p.N) ax[i] = f2bf(gelu_tanh(v[i]));
       }
     } else {
       float a[32];
@@ -120,8 +122,9 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off
       for (int i = 0; i < 8; ++i)
         c4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     } else {
-      for (int i = 0; i < 32 && n + i < p.N; ++i)
-        c[i] = v[i] + (p.beta != 0.f ? p.beta * c[i] : 0.f);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)   // static indices keep v[] in registers
+        if (n + i < p.N) c[i] = v[i] + (p.beta != 0.f ? p.beta * c[i] : 0.f);
     }
   } else {
     uint16_t* c = reinterpret_cast<uint16_t*>(p.C) + row_off + (int64_t)m * p.ldc + n;
@@ -145,9 +148,12 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off
                            pack_bf2(v[8 * i + 4], v[8 * i + 5]), pack_bf2(v[8 * i + 6], v[8 * i + 7]));
       }
     } else {
-      for (int i = 0; i < 32 && n + i < p.N; ++i) {
-        float o = (p.beta != 0.f) ? p.beta * bf2f(c[i]) : 0.f;
-        c[i] = f2bf(v[i] + o);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (n + i < p.N) {
+          float o = (p.beta != 0.f) ? p.beta * bf2f(c[i]) : 0.f;
+          c[i] = f2bf(v[i] + o);
+        }
       }
     }
   }
