@@ -136,14 +136,15 @@ def run_reference(args):
             vals.append((v, dt))
     v = statistics.median(x[0] for x in vals)
     dt = statistics.median(x[1] for x in vals)
-    plan = json.loads((ROOT / f"plans/gpt13b_n{args.gpus}/plan.json").read_text())
+    plan_path = Path(args.plan) if args.plan else ROOT / f"plans/gpt13b_n{args.gpus}/plan.json"
+    plan = json.loads(plan_path.read_text())
     step_flop = _plan_flop(plan)
     out = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_flop / (v * 1e12) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "impl": "reference",
-        "config": _config(args.gpus, plan),
+        "config": _config(args.gpus, plan, _rel(plan_path)),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": "oracle/dense.py numpy float32: 1 GPT-1.3B block x 1 microbatch "
                                    "(8 x 1024 tokens) fwd+bwd per step, %.2f s; ms_per_step "
@@ -160,7 +161,15 @@ def _plan_flop(doc) -> int:
     return per_mb * int(doc["num_microbatches"])
 
 
-def _config(n, doc):
+def _rel(p: Path) -> str:
+    p = Path(p).resolve()
+    try:
+        return str(p.relative_to(ROOT))
+    except ValueError:
+        return str(p)
+
+
+def _config(n, doc, plan_rel):
     stages = doc["stages"]
     return {
         "workload": "GPT-3 1.3B (24 blocks, h=2048, 32 heads, seq 1024) fwd+bwd+Adam, "
@@ -168,7 +177,7 @@ def _config(n, doc):
         "global_batch": SEQS_PER_MB * int(doc["num_microbatches"]),
         "seq_len": 1024, "microbatch_seqs": SEQS_PER_MB,
         "microbatches": int(doc["num_microbatches"]),
-        "plan": f"plans/gpt13b_n{n}/plan.json",
+        "plan": plan_rel,
         "parallelism": "+".join(f"stage{s['index']}:{s['logical_view'][0]}x{s['logical_view'][1]}"
                                 for s in stages),
         "schedule": "1f1b",
@@ -282,7 +291,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (N(0,1) inputs, random-init weights)",
-        "config": _config(args.gpus, doc),
+        "config": _config(args.gpus, doc, _rel(plan_path)),
         "frac_of_peak": {"measured_sustained": step_flop / t / 1e12 / (sus * args.gpus),
                          "datasheet_2250": step_flop / t / 1e12 / (2250.0 * args.gpus)},
         "roofline": {"bound": "tensor", "achieved": ach, "peak": sus, "unit": UNIT,

@@ -127,6 +127,27 @@ int mp_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                 void* dk, void* dv, int64_t B, int64_t H, int64_t s, int64_t d,
                 int64_t ld, float scale, void* stream);
 
+/* Key-range variants for stages that shard the softmax (key) dim of the
+ * scores over a mesh axis (spec RRS^a on the cluster's bmm/softmax nodes):
+ * only keys [kv0, kv0+kv_len) of every sequence are read (128-aligned).  fwd
+ * writes O / LSE normalised over that range; bwd writes dK / dV rows of the
+ * range and accumulates dq_acc over it, given the GLOBAL lse (and full O, dO). */
+int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void* o, float* lse,
+                   int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld, float scale,
+                   int64_t kv0, int64_t kv_len, void* stream);
+int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const void* o,
+                   const void* dout, const float* lse, float* dvec, float* dq_acc,
+                   void* dk, void* dv, int64_t B, int64_t H, int64_t s, int64_t d,
+                   int64_t ld, float scale, int64_t kv0, int64_t kv_len, void* stream);
+/* Combine of key-split partial attention (between the collectives over the key
+ * axis): scale: w = exp(lse - m), o *= w (m = max-allreduced lse);
+ * finish: o /= wsum, lse = m + log(wsum) (wsum = sum-allreduced w). */
+int mp_attn_combine_scale(void* o, const float* lse, const float* m, float* w, int64_t B,
+                          int64_t H, int64_t s, int64_t d, int64_t ld, void* stream);
+int mp_attn_combine_finish(void* o, const float* wsum, const float* m, float* lse,
+                           int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld,
+                           void* stream);
+
 /* ---- box pack / unpack (cross-mesh Transfer, reshard.py:32-37,97-108) -----
  * Copies the sub-box [lo, lo+ext) of a strided tensor of rank <= 4 to / from
  * a dense buffer.  dims/strides in elements, elem_bytes in {2,4}. */

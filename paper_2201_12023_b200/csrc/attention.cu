@@ -92,6 +92,7 @@ __device__ __forceinline__ void sts32(uint32_t a, float v) {
 
 struct FaFwdParams {
   int B, H, s, ld;
+  int kv0, nkv;      // key range: tiles [kv0/128, kv0/128 + nkv) of every sequence
   float scale_log2;  // log2(e) / sqrt(d)
   uint16_t* O;
   float* lse;        // [B*H, s]
@@ -131,8 +132,9 @@ __global__ void __launch_bounds__(192, 2)
   const int qt = blockIdx.x;                  // query tile
   const int bh = blockIdx.y;
   const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
-  const int n_kv = p.s / FA_BN;
+  const int n_kv = p.nkv;
   const int row0 = b * p.s;
+  const int krow0 = row0 + p.kv0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -166,10 +168,10 @@ __global__ void __launch_bounds__(192, 2)
         const int st = j & 1;
         mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[st], FA_TILE);
-        tma_load_2d(&tmK, &k_full[st], sK + st * FA_TILE, hh * FA_D, row0 + j * FA_BN);
+        tma_load_2d(&tmK, &k_full[st], sK + st * FA_TILE, hh * FA_D, krow0 + j * FA_BN);
         mbar_wait(v_empty, (j & 1) ^ 1);
         mbar_arrive_expect_tx(v_full, FA_TILE);
-        tma_load_2d(&tmV, v_full, sV, hh * FA_D, row0 + j * FA_BN);
+        tma_load_2d(&tmV, v_full, sV, hh * FA_D, krow0 + j * FA_BN);
       }
     }
   } else if (warp == 1) {
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(192, 2)
 // ------------------------------------------------------------------ backward
 struct FaBwdParams {
   int B, H, s, ld;
+  int kv0;            // first key of the range this grid covers (grid.x key tiles)
   float scale;        // 1/sqrt(d)
   const float* lse;   // [B*H, s]
   const float* dvec;  // D = rowsum(dO * O), [B*H, s]
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
   const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
   const int n_q = p.s / FA_BM;
   const int row0 = b * p.s;
+  const int krow0 = row0 + p.kv0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -412,8 +416,8 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       mbar_arrive_expect_tx(kv_full, 2 * FA_TILE);
-      tma_load_2d(&tmK, kv_full, sK, hh * FA_D, row0 + kt * FA_BN);
-      tma_load_2d(&tmV, kv_full, sV, hh * FA_D, row0 + kt * FA_BN);
+      tma_load_2d(&tmK, kv_full, sK, hh * FA_D, krow0 + kt * FA_BN);
+      tma_load_2d(&tmV, kv_full, sV, hh * FA_D, krow0 + kt * FA_BN);
     }
     for (int i = 0; i < n_q; ++i) {
       const int st = i & 1;
@@ -545,7 +549,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     // dK (half 0) / dV (half 1) epilogue: key row r
     mbar_wait(acc_done, 0);
     tc_fence_after();
-    const int64_t grow = row0 + kt * FA_BN + r;
+    const int64_t grow = krow0 + kt * FA_BN + r;
     const uint32_t tacc = half ? tdV : tdK;
     uint16_t* out = (half ? p.dV : p.dK) + grow * p.ld + hh * FA_D;
 #pragma unroll
@@ -622,6 +626,44 @@ __global__ void fa_bwd_pre_kernel(const uint16_t* __restrict__ O, const uint16_t
   }
 }
 
+// Key-split attention (keys sharded over a mesh axis): each device holds O and
+// LSE over its own keys; with M = max over devices of LSE, w = exp(LSE - M),
+// O = sum(w * O_loc) / sum(w) and LSE = M + log(sum w).  Warp per (bh, t) row.
+__global__ void attn_combine_scale_kernel(uint16_t* __restrict__ O, const float* __restrict__ lse,
+                                          const float* __restrict__ m, float* __restrict__ w,
+                                          int B, int H, int s, int ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)B * H * s;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb) {
+    const int64_t bh = r / s, t = r - (r / s) * s;
+    const int64_t b = bh / H, hh = bh - (bh / H) * H;
+    const float wt = __expf(lse[r] - m[r]);
+    uint32_t* o = reinterpret_cast<uint32_t*>(O + (b * s + t) * ld + hh * FA_D) + lane;
+    const uint32_t v = *o;
+    *o = pack_bf2(bf2f(v & 0xffff) * wt, bf2f(v >> 16) * wt);
+    if (lane == 0) w[r] = wt;
+  }
+}
+
+__global__ void attn_combine_finish_kernel(uint16_t* __restrict__ O, const float* __restrict__ wsum,
+                                           const float* __restrict__ m, float* __restrict__ lse,
+                                           int B, int H, int s, int ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = (int64_t)B * H * s;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < rows; r += (int64_t)gridDim.x * wpb) {
+    const int64_t bh = r / s, t = r - (r / s) * s;
+    const int64_t b = bh / H, hh = bh - (bh / H) * H;
+    const float ws = wsum[r];
+    const float inv = 1.f / ws;
+    uint32_t* o = reinterpret_cast<uint32_t*>(O + (b * s + t) * ld + hh * FA_D) + lane;
+    const uint32_t v = *o;
+    *o = pack_bf2(bf2f(v & 0xffff) * inv, bf2f(v >> 16) * inv);
+    if (lane == 0) lse[r] = m[r] + __logf(ws);
+  }
+}
+
 // ------------------------------------------------------------------ host
 static PFN_cuTensorMapEncodeTiled_v12000 fa_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -664,12 +706,20 @@ static bool fa_args_ok(const void* p, int64_t ld) {
 
 using namespace mp;
 
-extern "C" int mp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
-                           int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld, float scale,
-                           void* stream) {
+static unsigned row_warps_grid(int64_t rows) {
+  int64_t blocks = (rows * 32 + 255) / 256;
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  return (unsigned)(blocks > 0 ? blocks : 1);
+}
+
+extern "C" int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void* o, float* lse,
+                              int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld, float scale,
+                              int64_t kv0, int64_t kv_len, void* stream) {
   clear_error();
   MP_CHECK_ARG(d == FA_D, "head dim must be 64");
   MP_CHECK_ARG(s % 128 == 0 && s > 0, "sequence length must be a multiple of 128");
+  MP_CHECK_ARG(kv0 % 128 == 0 && kv_len % 128 == 0 && kv_len > 0 && kv0 >= 0 && kv0 + kv_len <= s,
+               "key range must be 128-aligned and inside the sequence");
   MP_CHECK_ARG(ld >= H * d, "row stride smaller than heads*d");
   MP_CHECK_ARG(fa_args_ok(q, ld) && fa_args_ok(k, ld) && fa_args_ok(v, ld) && fa_args_ok(o, ld) &&
                    lse,
@@ -684,35 +734,38 @@ extern "C" int mp_attn_fwd(const void* q, const void* k, const void* v, void* o,
     cudaFuncSetAttribute(fa_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_FWD_SMEM);
     configured = true;
   }
-  FaFwdParams p{(int)B, (int)H, (int)s, (int)ld, scale * 1.4426950408889634f,
-                reinterpret_cast<uint16_t*>(o), lse};
+  FaFwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, (int)(kv_len / FA_BN),
+                scale * 1.4426950408889634f, reinterpret_cast<uint16_t*>(o), lse};
   dim3 grid((unsigned)(s / FA_BM), (unsigned)(B * H));
   fa_fwd_kernel<<<grid, 192, FA_FWD_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, p);
   MP_CHECK_LAUNCH();
   return 0;
 }
 
-extern "C" int mp_attn_bwd(const void* q, const void* k, const void* v, const void* o,
-                           const void* dout, const float* lse, float* dvec, float* dq_acc,
-                           void* dk, void* dv, int64_t B, int64_t H, int64_t s, int64_t d,
-                           int64_t ld, float scale, void* stream) {
+extern "C" int mp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                           int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld, float scale,
+                           void* stream) {
+  return mp_attn_fwd_kv(q, k, v, o, lse, B, H, s, d, ld, scale, 0, s, stream);
+}
+
+extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const void* o,
+                              const void* dout, const float* lse, float* dvec, float* dq_acc,
+                              void* dk, void* dv, int64_t B, int64_t H, int64_t s, int64_t d,
+                              int64_t ld, float scale, int64_t kv0, int64_t kv_len, void* stream) {
   clear_error();
   MP_CHECK_ARG(d == FA_D, "head dim must be 64");
   MP_CHECK_ARG(s % 128 == 0 && s > 0, "sequence length must be a multiple of 128");
+  MP_CHECK_ARG(kv0 % 128 == 0 && kv_len % 128 == 0 && kv_len > 0 && kv0 >= 0 && kv0 + kv_len <= s,
+               "key range must be 128-aligned and inside the sequence");
   MP_CHECK_ARG(fa_args_ok(q, ld) && fa_args_ok(k, ld) && fa_args_ok(v, ld) && fa_args_ok(o, ld) &&
                    fa_args_ok(dout, ld) && fa_args_ok(dk, ld) && fa_args_ok(dv, ld) && lse &&
                    dvec && dq_acc,
                "bad pointers");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  {
-    const int64_t rows = B * H * s;
-    int64_t blocks = (rows * 32 + 255) / 256;
-    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
-    fa_bwd_pre_kernel<<<(unsigned)blocks, 256, 0, st>>>(
-        reinterpret_cast<const uint16_t*>(o), reinterpret_cast<const uint16_t*>(dout), dvec,
-        (int)B, (int)H, (int)s, (int)ld);
-    MP_CHECK_LAUNCH();
-  }
+  fa_bwd_pre_kernel<<<row_warps_grid(B * H * s), 256, 0, st>>>(
+      reinterpret_cast<const uint16_t*>(o), reinterpret_cast<const uint16_t*>(dout), dvec, (int)B,
+      (int)H, (int)s, (int)ld);
+  MP_CHECK_LAUNCH();
   CUtensorMap mq, mk, mv, mdo;
   int rc;
   if ((rc = fa_map(&mq, q, B * s, ld)) || (rc = fa_map(&mk, k, B * s, ld)) ||
@@ -723,10 +776,41 @@ extern "C" int mp_attn_bwd(const void* q, const void* k, const void* v, const vo
     cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_BWD_SMEM);
     configured = true;
   }
-  FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, scale, lse, dvec, dq_acc,
+  FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, scale, lse, dvec, dq_acc,
                 reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
-  dim3 grid((unsigned)(s / FA_BN), (unsigned)(B * H));
+  dim3 grid((unsigned)(kv_len / FA_BN), (unsigned)(B * H));
   fa_bwd_kernel<<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, p);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int mp_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                           const void* dout, const float* lse, float* dvec, float* dq_acc,
+                           void* dk, void* dv, int64_t B, int64_t H, int64_t s, int64_t d,
+                           int64_t ld, float scale, void* stream) {
+  return mp_attn_bwd_kv(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, B, H, s, d, ld, scale, 0, s,
+                        stream);
+}
+
+extern "C" int mp_attn_combine_scale(void* o, const float* lse, const float* m, float* w, int64_t B,
+                                     int64_t H, int64_t s, int64_t d, int64_t ld, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(d == FA_D && fa_args_ok(o, ld) && lse && m && w, "bad arguments");
+  attn_combine_scale_kernel<<<row_warps_grid(B * H * s), 256, 0,
+                              reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint16_t*>(o), lse, m, w, (int)B, (int)H, (int)s, (int)ld);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+extern "C" int mp_attn_combine_finish(void* o, const float* wsum, const float* m, float* lse,
+                                      int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld,
+                                      void* stream) {
+  clear_error();
+  MP_CHECK_ARG(d == FA_D && fa_args_ok(o, ld) && wsum && m && lse, "bad arguments");
+  attn_combine_finish_kernel<<<row_warps_grid(B * H * s), 256, 0,
+                               reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint16_t*>(o), wsum, m, lse, (int)B, (int)H, (int)s, (int)ld);
   MP_CHECK_LAUNCH();
   return 0;
 }

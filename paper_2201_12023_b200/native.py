@@ -46,6 +46,14 @@ EXPORTS = {
                      c_vp], c_int),
     "mp_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
                      c_i64, c_i64, c_i64, c_f32, c_vp], c_int),
+    "mp_attn_fwd_kv": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_f32,
+                        c_i64, c_i64, c_vp], c_int),
+    "mp_attn_bwd_kv": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
+                        c_i64, c_i64, c_i64, c_i64, c_f32, c_i64, c_i64, c_vp], c_int),
+    "mp_attn_combine_scale": ([c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp],
+                              c_int),
+    "mp_attn_combine_finish": ([c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp],
+                               c_int),
     "mp_nccl_version": ([], c_int),
     "mp_nccl_unique_id": ([c_vp], c_int),
     "mp_comm_init": ([c_vp, c_int, c_int, ctypes.POINTER(c_vp)], c_int),
@@ -333,28 +341,52 @@ def _heads_view(t: torch.Tensor, name: str):
     return t.data_ptr(), t.stride(0)
 
 
-def attn_fwd(q, k, v, o, lse, B: int, H: int, s: int, d: int, scale: float, stream=None):
-    """Fused non-causal attention forward on (B*s, H*d) tensors; lse fp32 [B*H, s]."""
+def attn_fwd(q, k, v, o, lse, B: int, H: int, s: int, d: int, scale: float, stream=None,
+             kv_range=None):
+    """Fused non-causal attention forward on (B*s, H*d) tensors; lse fp32 [B*H, s].
+    kv_range=(kv0, kv_len) restricts the keys (O / lse then cover that range)."""
     ptrs = [_heads_view(t, n) for t, n in ((q, "q"), (k, "k"), (v, "v"), (o, "o"))]
     lds = {ld for _, ld in ptrs}
     if len(lds) != 1:
         raise NativeError("q/k/v/o must share the row stride")
     _require(lse, torch.float32, "lse")
-    _check(load().mp_attn_fwd(ptrs[0][0], ptrs[1][0], ptrs[2][0], ptrs[3][0], lse.data_ptr(),
-                              B, H, s, d, lds.pop(), float(scale), _stream(stream)), "mp_attn_fwd")
+    kv0, kvl = kv_range if kv_range is not None else (0, s)
+    _check(load().mp_attn_fwd_kv(ptrs[0][0], ptrs[1][0], ptrs[2][0], ptrs[3][0], lse.data_ptr(),
+                                 B, H, s, d, lds.pop(), float(scale), kv0, kvl, _stream(stream)),
+           "mp_attn_fwd")
 
 
 def attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, B: int, H: int, s: int, d: int,
-             scale: float, stream=None):
+             scale: float, stream=None, kv_range=None):
     ptrs = [_heads_view(t, n) for t, n in ((q, "q"), (k, "k"), (v, "v"), (o, "o"), (dout, "dout"),
                                             (dk, "dk"), (dv, "dv"))]
     lds = {ld for _, ld in ptrs} | {dq_acc.stride(0)}
     if len(lds) != 1:
         raise NativeError("attention operands must share the row stride")
-    _check(load().mp_attn_bwd(ptrs[0][0], ptrs[1][0], ptrs[2][0], ptrs[3][0], ptrs[4][0],
-                              lse.data_ptr(), dvec.data_ptr(), dq_acc.data_ptr(), ptrs[5][0],
-                              ptrs[6][0], B, H, s, d, lds.pop(), float(scale), _stream(stream)),
+    kv0, kvl = kv_range if kv_range is not None else (0, s)
+    _check(load().mp_attn_bwd_kv(ptrs[0][0], ptrs[1][0], ptrs[2][0], ptrs[3][0], ptrs[4][0],
+                                 lse.data_ptr(), dvec.data_ptr(), dq_acc.data_ptr(), ptrs[5][0],
+                                 ptrs[6][0], B, H, s, d, lds.pop(), float(scale), kv0, kvl,
+                                 _stream(stream)),
            "mp_attn_bwd")
+
+
+def attn_combine_scale(o, lse, m, w, B: int, H: int, s: int, d: int, stream=None):
+    """Key-split combine, step 1: w = exp(lse - m); o *= w (row-wise per head)."""
+    p, ld = _heads_view(o, "o")
+    for t, n in ((lse, "lse"), (m, "m"), (w, "w")):
+        _require(t, torch.float32, n)
+    _check(load().mp_attn_combine_scale(p, lse.data_ptr(), m.data_ptr(), w.data_ptr(), B, H, s, d,
+                                        ld, _stream(stream)), "mp_attn_combine_scale")
+
+
+def attn_combine_finish(o, wsum, m, lse, B: int, H: int, s: int, d: int, stream=None):
+    """Key-split combine, step 2: o /= wsum; lse = m + log(wsum)."""
+    p, ld = _heads_view(o, "o")
+    for t, n in ((wsum, "wsum"), (m, "m"), (lse, "lse")):
+        _require(t, torch.float32, n)
+    _check(load().mp_attn_combine_finish(p, wsum.data_ptr(), m.data_ptr(), lse.data_ptr(), B, H, s,
+                                         d, ld, _stream(stream)), "mp_attn_combine_finish")
 
 
 # --------------------------------------------------------------------------- boxes

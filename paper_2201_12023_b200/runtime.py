@@ -66,6 +66,7 @@ class ExecResult:
     params: Optional[dict[int, np.ndarray]] = None
     outputs: Optional[dict] = None                  # (microbatch, node) -> global forward output
     gpu_launches: int = 0
+    fused: dict = field(default_factory=dict)       # this rank's stage: fused clusters / epilogues
 
 
 @dataclass
@@ -325,9 +326,19 @@ class StageRunner:
             if b[gC].op != "split" or g[dprobs].inputs[0] != gC:
                 continue
             nodes = [S, P, C, qh, kh, vh, gC] + bwd
-            local = self.mesh.size == 1 or all(self.spec(n).is_replicated() for n in nodes)
-            if not local or any(n in self.st.output_specs for n in [S, P, C] + bwd):
+            if any(n in self.st.output_specs for n in [S, P, C] + bwd):
                 continue
+            key_axes: tuple[int, ...] = ()
+            if not (self.mesh.size == 1 or all(self.spec(n).is_replicated() for n in nodes)):
+                # keys sharded: scores / probs RRS^A over replicated q, k, v, dctx
+                ss = self.spec(S)
+                if (ss != self.spec(P) or ss.dims[0] or ss.dims[1] or not ss.dims[2]
+                        or not all(self.spec(n).is_replicated() for n in (qh, kh, vh, gC))):
+                    continue
+                key_axes = tuple(ss.dims[2])
+                k0, k1 = device_box(g[S].dims, ss, self.mesh, self.me)[2]
+                if k0 % 128 or (k1 - k0) % 128:
+                    continue
             # every cluster output consumed only inside the cluster or by one merge
             outs_ok = True
             for n, want in ((C, "merge"), (dqh, "merge"), (dkh, "merge_t"), (dvh, "merge")):
@@ -339,7 +350,9 @@ class StageRunner:
             cl = dict(S=S, P=P, C=C, qh=qh, kh=kh, vh=vh, gC=gC, dqh=dqh, dkh=dkh, dvh=dvh,
                       q=g[qh].inputs[0], k=g[kh].inputs[0], v=g[vh].inputs[0],
                       dctx2=g[gC].inputs[0], heads=(Bn, H, sq, d),
-                      scale=b[P].softmax_scale, bwd=set(bwd))
+                      scale=b[P].softmax_scale, bwd=set(bwd), key_axes=key_axes,
+                      kv=(device_box(g[S].dims, self.spec(S), self.mesh, self.me)[2]
+                          if key_axes else (0, sq)))
             clusters.append(cl)
         for cl in clusters:
             fwd_ops = []
@@ -368,6 +381,11 @@ class StageRunner:
         return clusters
 
     def _run_attn_fwd(self, mb: int, op: _Op):
+        """Fused attention forward.  With the keys sharded over mesh axes A
+        (cluster['key_axes']), each device attends over its own key block, then
+        O and LSE are combined across A: M = max LSE, w = exp(LSE - M),
+        O = sum(w O) / sum(w), LSE = M + log sum(w) (two all-reduces) — the
+        plan's own RRS^A scores / probs are never materialised."""
         cl = op.extra
         Bn, H, s, d = cl["heads"]
         rep = replicated(2)
@@ -376,11 +394,25 @@ class StageRunner:
         v = self._contig(self.get(mb, cl["v"], rep))
         o = torch.empty(Bn * s, H * d, dtype=torch.bfloat16, device=self.dev)
         lse = torch.empty(Bn * H, s, dtype=torch.float32, device=self.dev)
-        native.attn_fwd(q, k, v, o, lse, Bn, H, s, d, cl["scale"])
+        k0, k1 = cl["kv"]
+        native.attn_fwd(q, k, v, o, lse, Bn, H, s, d, cl["scale"], kv_range=(k0, k1 - k0))
+        if cl["key_axes"]:
+            axes = cl["key_axes"]
+            m = lse.clone()
+            self._allreduce(m, axes, dist.ReduceOp.MAX)
+            w = torch.empty_like(lse)
+            native.attn_combine_scale(o, lse, m, w, Bn, H, s, d)
+            self._allreduce(o, axes)
+            self._allreduce(w, axes)
+            native.attn_combine_finish(o, w, m, lse, Bn, H, s, d)
         self.aux.setdefault(mb, {})[cl["S"]] = (o, lse)
-        return o.view(Bn, s, H, d).permute(0, 2, 1, 3)       # logical ctx (B*H, s, d)
+        ctx = o.view(Bn, s, H, d).permute(0, 2, 1, 3)        # logical ctx (B*H, s, d)
+        return self._coerce(ctx, self.graph[cl["C"]].dims, replicated(3), self.spec(cl["C"]))
 
     def _run_attn_bwd(self, mb: int, op: _Op):
+        """Fused attention backward.  Key-split: dQ partial sums over the local
+        keys are all-reduced across the key axes; dK / dV come out for the
+        local keys (RRS^A / RS^AR), then reach the nodes' own specs."""
         cl = op.extra
         Bn, H, s, d = cl["heads"]
         rep = replicated(2)
@@ -390,17 +422,49 @@ class StageRunner:
         dout = self._contig(self.get(mb, cl["dctx2"], rep))
         o, lse = self.aux[mb][cl["S"]]
         T, hdim = Bn * s, H * d
+        k0, k1 = cl["kv"]
         dvec = torch.empty(Bn * H, s, dtype=torch.float32, device=self.dev)
         dq_acc = torch.zeros(T, hdim, dtype=torch.float32, device=self.dev)
         dk = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
         dv = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
-        native.attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, Bn, H, s, d, cl["scale"])
+        native.attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, Bn, H, s, d, cl["scale"],
+                        kv_range=(k0, k1 - k0))
         dq = native.cast_f32_bf16(dq_acc, torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev))
+        g = self.graph
         vals = self.vals[mb]
-        vals[cl["dqh"]] = dq.view(Bn, s, H, d).permute(0, 2, 1, 3)
-        vals[cl["dkh"]] = dk.view(Bn, s, H, d).permute(0, 2, 3, 1)
-        vals[cl["dvh"]] = dv.view(Bn, s, H, d).permute(0, 2, 1, 3)
+        axes = cl["key_axes"]
+        if axes:
+            self._allreduce(dq, axes)
+            ks = Spec(((), (), axes))
+            vs = Spec(((), axes, ()))
+        else:
+            ks = vs = replicated(3)
+        vals[cl["dqh"]] = self._coerce(dq.view(Bn, s, H, d).permute(0, 2, 1, 3), g[cl["dqh"]].dims,
+                                       replicated(3), self.spec(cl["dqh"]))
+        dk4 = dk.view(Bn, s, H, d).permute(0, 2, 3, 1)
+        dv4 = dv.view(Bn, s, H, d).permute(0, 2, 1, 3)
+        if axes:
+            dk4 = dk4.narrow(3, k0, k1 - k0)
+            dv4 = dv4.narrow(2, k0, k1 - k0)
+        vals[cl["dkh"]] = self._coerce(dk4, g[cl["dkh"]].dims, ks, self.spec(cl["dkh"]))
+        vals[cl["dvh"]] = self._coerce(dv4, g[cl["dvh"]].dims, vs, self.spec(cl["dvh"]))
         return None
+
+    def _coerce(self, v: torch.Tensor, dims, have: Spec, req: Spec) -> torch.Tensor:
+        """A local value in layout `have` brought to layout `req` (no cache)."""
+        have, req = canonical(have, self.mesh), canonical(req, self.mesh)
+        if have == req:
+            return v
+        kind, info = self._relayout_plan(tuple(dims), have, req)
+        if kind == "local":
+            return self._narrow(v, info)
+        if kind == "allgather":
+            out = torch.empty(local_dims(dims, req, self.mesh), dtype=v.dtype, device=self.dev)
+            src = self._contig(self._as3(v))
+            self.comm.all_gather_into(out.view(-1), src.view(-1),
+                                      self.comm.axis_group(self.st.index, self.mesh, info, self.me))
+            return out
+        return self._relayout(self._as3(v), tuple(dims), have, req)
 
     # ------------------------------------------------------------------ params
     def _init_params(self, init: Optional[dict[int, np.ndarray]]):
@@ -477,17 +541,7 @@ class StageRunner:
         c = self.cache.setdefault(mb, {})
         if key in c:
             return c[key]
-        dims = self.graph[nid].dims
-        kind, info = self._relayout_plan(dims, have, req)
-        if kind == "local":
-            out = self._narrow(v, info)
-        elif kind == "allgather":
-            out = torch.empty(local_dims(dims, req, self.mesh), dtype=v.dtype, device=self.dev)
-            src = self._contig(self._as3(v))
-            self.comm.all_gather_into(out.view(-1), src.view(-1),
-                                      self.comm.axis_group(self.st.index, self.mesh, info, self.me))
-        else:
-            out = self._relayout(self._as3(v), dims, have, req)
+        out = self._coerce(v, self.graph[nid].dims, have, req)
         c[key] = out
         return out
 
@@ -1102,9 +1156,14 @@ class Executor:
         busy = sum(e - s for ins, s, e in evs if ins.op in ("compute", "send", "all_gather"))
         util = {self.runner.st.index: busy / makespan if makespan > 0 else 0.0}
         peak = {self.rank: int(torch.cuda.max_memory_allocated())}
+        r = self.runner
         return ExecResult(makespan=makespan, utilization=util, peak_bytes=peak, events=events,
                           loss=self.loss(), step_times=list(self.step_times), grads=grads,
-                          outputs=outputs, gpu_launches=launches)
+                          outputs=outputs, gpu_launches=launches,
+                          fused={"attention": len(r.attn_clusters),
+                                 "attention_key_split": sum(1 for c in r.attn_clusters
+                                                            if c["key_axes"]),
+                                 "epilogues": r.fused_epilogues})
 
 
 def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, steps: int = 1,

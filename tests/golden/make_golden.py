@@ -49,8 +49,9 @@ def concrete(n, m, first):
 
 def dump(path: Path, obj):
     path.parent.mkdir(parents=True, exist_ok=True)
-    with gzip.open(path, "wt") as f:
-        json.dump(obj, f, sort_keys=True, separators=(",", ":"))
+    data = json.dumps(obj, sort_keys=True, separators=(",", ":")).encode()
+    with open(path, "wb") as raw, gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as f:
+        f.write(data)   # mtime=0: regenerating unchanged fixtures leaves them byte-identical
 
 
 def xmesh_case(dims, eb, sv, ss, dv, ds, opt):

@@ -15,10 +15,11 @@ from parity_harness import ROOT, TOL, run_plan
 
 pytestmark = pytest.mark.gpu
 
-SINGLE = ["plans/mlp_n1/plan.json", "plans/tiny_gpt_n1/plan.json"]
+SINGLE = ["plans/mlp_n1/plan.json", "plans/tiny_gpt_n1/plan.json",
+          "plans/tiny_gpt_deep_n1/plan.json"]
 MULTI = [("plans/mlp_n2/plan.json", 2), ("plans/tiny_gpt_n2/plan.json", 2),
          ("plans/tiny_gpt_n4/plan.json", 4), ("plans/cfg1/plan.json", 4),
-         ("plans/tiny_gpt_n8/plan.json", 8)]
+         ("plans/tiny_gpt_n8/plan.json", 8), ("plans/tiny_gpt_tp_n4/plan.json", 4)]
 
 
 @pytest.mark.parametrize("plan", SINGLE)
@@ -28,7 +29,7 @@ def test_single_device_parity(plan, schedule):
     print(json.dumps(errs))
     assert errs["loss"] <= TOL["loss"], errs
     assert errs["output"] <= TOL["output"], errs
-    assert errs["grad"] <= TOL["grad"], errs
+    assert errs["ok"], errs
     assert errs["gpu_launches"] > 0
 
 
@@ -45,3 +46,5 @@ def test_multi_device_parity(plan, n):
     assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
     errs = json.loads(lines[-1])
     assert errs["ok"], errs
+    if "tiny_gpt_tp" in plan:   # GPT-1.3B's (1,2) key-split attention, shrunk
+        assert errs["fused"]["attention_key_split"] > 0, errs
