@@ -224,7 +224,10 @@ class StageRunner:
         # fwd output of the graph (for the loss seed / checks)
         self.seed_ids = [o.nid for o in self.bwd_ops if o.op == "seed"]
         self.members = members
+        # values stored in a layout other than the plan's (fused-cluster outputs)
+        self.actual: dict[int, Spec] = {}
         self.fuse_attention = os.environ.get("MPEXEC_FUSE_ATTENTION", "1") != "0"
+        self.force_key_split = os.environ.get("MPEXEC_ATTN_KEY_SPLIT", "0") == "1"
         self.attn_clusters = self._fuse_attention() if self.fuse_attention else []
         self.fused_epilogues = (self._fuse_epilogues()
                                 if os.environ.get("MPEXEC_FUSE_EPILOGUE", "1") != "0" else 0)
@@ -275,10 +278,23 @@ class StageRunner:
     # ------------------------------------------------------------------ fusion
     def _fuse_attention(self) -> list[dict]:
         """Replace each eligible attention cluster (graph.py:297-302 and its
-        backward, graph.py:341-361) by the fused tcgen05 kernels.  Eligible when
-        every node of the cluster is local to the device (stage of one device or
-        all-replicated specs: the softmax dim is then local) and d = 64,
-        s % 128 == 0.  Returns the clusters fused."""
+        backward, graph.py:341-361) by the fused tcgen05 kernels (d = 64,
+        s % 128 == 0).  The cluster's interior (head splits, scores, probs,
+        their transposes and gradients) is never materialised, so the executor
+        is free to pick how the work is split across the stage's devices; the
+        values leaving the cluster are bit-for-bit the same tensors:
+
+          local  q, k, v, dctx brought to one common (T, h) layout whose every
+                 device tile is whole sequences x whole heads (batch split,
+                 head split, or replicated): attention runs on the local tile
+                 with no communication, and the head merges of ctx / dq / dk /
+                 dv are produced directly in that layout (their consumers
+                 reshard on demand, runtime.get)
+          keys   the plan shards the key dim of scores / probs (RRS^A) over
+                 replicated q, k, v: attention over the local key block, LSE
+                 combine across A (see _run_attn_fwd)
+
+        Returns the clusters fused."""
         g = self.graph
         b = self.bound
         cons = self.cons
@@ -310,9 +326,6 @@ class StageRunner:
             if d != 64 or sq % 128 or b[kh].heads != (Bn, H, sq, d) or b[vh].heads != (Bn, H, sq, d):
                 continue
             bwd = sorted(colo.get(C, []) + colo.get(P, []) + colo.get(S, []))
-            byk = {}
-            for nid in bwd:
-                byk.setdefault(b[nid].op, []).append(nid)
             try:
                 dprobs = [n for n in colo.get(C, []) if b[n].op == "bmm" and g[n].inputs[0] != P
                           and b[g[n].inputs[1]].op == "transpose"][0]
@@ -325,69 +338,129 @@ class StageRunner:
             gC = g[dvh].inputs[1]                  # dL/dctx (a head split of dL/dctx2)
             if b[gC].op != "split" or g[dprobs].inputs[0] != gC:
                 continue
-            nodes = [S, P, C, qh, kh, vh, gC] + bwd
-            if any(n in self.st.output_specs for n in [S, P, C] + bwd):
+            inner = set([S, P, C] + bwd)
+            if any(n in self.st.output_specs for n in inner):
                 continue
-            key_axes: tuple[int, ...] = ()
-            if not (self.mesh.size == 1 or all(self.spec(n).is_replicated() for n in nodes)):
+            # every cluster output consumed only by one head merge
+            merges = {}
+            for n, want in ((C, "merge"), (dqh, "merge"), (dkh, "merge_t"), (dvh, "merge")):
+                users = [c for c, _ in cons[n] if c not in inner]
+                if len(users) != 1 or b[users[0]].op != want or users[0] not in self.members:
+                    break
+                merges[n] = users[0]
+            if len(merges) != 4:
+                continue
+            q, k, v = g[qh].inputs[0], g[kh].inputs[0], g[vh].inputs[0]
+            dctx2 = g[gC].inputs[0]
+            # head splits whose only consumers are inside the cluster are dropped
+            splits = [x for x in (qh, kh, vh, gC)
+                      if all(c in inner for c, _ in cons[x]) and x not in self.st.output_specs]
+            cl = dict(S=S, P=P, C=C, qh=qh, kh=kh, vh=vh, gC=gC, dqh=dqh, dkh=dkh, dvh=dvh,
+                      q=q, k=k, v=v, dctx2=dctx2, heads=(Bn, H, sq, d),
+                      scale=b[P].softmax_scale, bwd=set(bwd), splits=set(splits),
+                      merges=merges, key_axes=(), kv=(0, sq), local=None)
+            local = self._attn_local_spec([q, k, v, dctx2], Bn, H, sq, d)
+            if self.force_key_split and self.spec(S).dims[2]:
+                local = None            # test hook: exercise the key-split path
+            if local is not None and (not local.is_replicated() or self.mesh.size == 1 or
+                                      all(self.spec(n).is_replicated()
+                                          for n in [S, P, C, qh, kh, vh, gC] + bwd)):
+                cl["local"] = local
+            else:
                 # keys sharded: scores / probs RRS^A over replicated q, k, v, dctx
                 ss = self.spec(S)
                 if (ss != self.spec(P) or ss.dims[0] or ss.dims[1] or not ss.dims[2]
                         or not all(self.spec(n).is_replicated() for n in (qh, kh, vh, gC))):
                     continue
-                key_axes = tuple(ss.dims[2])
-                k0, k1 = device_box(g[S].dims, ss, self.mesh, self.me)[2]
-                if k0 % 128 or (k1 - k0) % 128:
+                ok = True
+                for dev in self._stage_devices():
+                    k0, k1 = device_box(g[S].dims, ss, self.mesh, dev)[2]
+                    ok &= k0 % 128 == 0 and (k1 - k0) % 128 == 0 and k1 > k0
+                if not ok:
                     continue
-            # every cluster output consumed only inside the cluster or by one merge
-            outs_ok = True
-            for n, want in ((C, "merge"), (dqh, "merge"), (dkh, "merge_t"), (dvh, "merge")):
-                users = [c for c, _ in cons[n] if c not in bwd]
-                if len(users) != 1 or b[users[0]].op != want:
-                    outs_ok = False
-            if not outs_ok:
-                continue
-            cl = dict(S=S, P=P, C=C, qh=qh, kh=kh, vh=vh, gC=gC, dqh=dqh, dkh=dkh, dvh=dvh,
-                      q=g[qh].inputs[0], k=g[kh].inputs[0], v=g[vh].inputs[0],
-                      dctx2=g[gC].inputs[0], heads=(Bn, H, sq, d),
-                      scale=b[P].softmax_scale, bwd=set(bwd), key_axes=key_axes,
-                      kv=(device_box(g[S].dims, self.spec(S), self.mesh, self.me)[2]
-                          if key_axes else (0, sq)))
+                cl["key_axes"] = tuple(ss.dims[2])
+                cl["kv"] = device_box(g[S].dims, ss, self.mesh, self.me)[2]
             clusters.append(cl)
         for cl in clusters:
+            local = cl["local"] is not None
+            drop_f = {cl["S"], cl["P"], cl["C"]} | (cl["splits"] & {cl["qh"], cl["kh"], cl["vh"]})
+            drop_b = set(cl["bwd"]) | (cl["splits"] & {cl["gC"]})
+            if local:
+                drop_f.add(cl["merges"][cl["C"]])
+                drop_b |= {cl["merges"][n] for n in (cl["dqh"], cl["dkh"], cl["dvh"])}
             fwd_ops = []
             for o in self.fwd_ops:
                 if o.nid == cl["S"]:
-                    fo = _Op(cl["C"], "attn_fwd", self.bound[cl["C"]], [], self.spec(cl["C"]))
+                    nid = cl["merges"][cl["C"]] if local else cl["C"]
+                    fo = _Op(nid, "attn_fwd", self.bound[nid], [], self.spec(nid))
                     fo.extra = cl
                     fwd_ops.append(fo)
-                elif o.nid in (cl["P"], cl["C"]):
-                    continue
-                else:
+                elif o.nid not in drop_f:
                     fwd_ops.append(o)
             self.fwd_ops = fwd_ops
             bwd_ops = []
             placed = False
             for o in self.bwd_ops:
-                if o.nid in cl["bwd"]:
-                    if not placed:
-                        bo = _Op(cl["dqh"], "attn_bwd", self.bound[cl["dqh"]], [], self.spec(cl["dqh"]))
-                        bo.extra = cl
-                        bwd_ops.append(bo)
-                        placed = True
-                    continue
-                bwd_ops.append(o)
+                if o.nid in cl["bwd"] and not placed:
+                    bo = _Op(cl["dqh"], "attn_bwd", self.bound[cl["dqh"]], [], self.spec(cl["dqh"]))
+                    bo.extra = cl
+                    bwd_ops.append(bo)
+                    placed = True
+                if o.nid not in drop_b:
+                    bwd_ops.append(o)
             self.bwd_ops = bwd_ops
+            if local:
+                for n in (cl["C"], cl["dqh"], cl["dkh"], cl["dvh"]):
+                    m = cl["merges"][n]
+                    if m not in self.out_ids:
+                        self.actual[m] = cl["local"]
         return clusters
 
+    def _stage_devices(self) -> list[int]:
+        return list(self.mesh.device_ids)
+
+    def _attn_local_spec(self, nids, B: int, H: int, s: int, d: int) -> Optional[Spec]:
+        """A (T, h) layout, taken from the attention inputs' own specs (most
+        common first), in which every device of the stage holds whole sequences
+        x whole heads; None if there is none."""
+        specs = [self.spec(n) for n in nids]
+        order = sorted(dict.fromkeys(specs), key=lambda sp: (-specs.count(sp), specs.index(sp)))
+        dims = (B * s, H * d)
+        for sp in order:
+            if len(sp.dims) != 2:
+                continue
+            ok = True
+            for dev in self._stage_devices():
+                (r0, r1), (c0, c1) = device_box(dims, sp, self.mesh, dev)
+                ok &= (r0 % s == 0 and (r1 - r0) % s == 0 and r1 > r0 and
+                       c0 % d == 0 and (c1 - c0) % d == 0 and c1 > c0)
+            if ok:
+                return sp
+        return None
+
     def _run_attn_fwd(self, mb: int, op: _Op):
-        """Fused attention forward.  With the keys sharded over mesh axes A
-        (cluster['key_axes']), each device attends over its own key block, then
-        O and LSE are combined across A: M = max LSE, w = exp(LSE - M),
-        O = sum(w O) / sum(w), LSE = M + log sum(w) (two all-reduces) — the
-        plan's own RRS^A scores / probs are never materialised."""
+        """Fused attention forward.  local: the device's tile of whole
+        sequences x heads, no communication.  keys: each device attends over
+        its own key block, then O and LSE are combined across the key axes A:
+        M = max LSE, w = exp(LSE - M), O = sum(w O) / sum(w),
+        LSE = M + log sum(w) (two all-reduces) — the plan's RRS^A scores /
+        probs are never materialised."""
         cl = op.extra
         Bn, H, s, d = cl["heads"]
+        if cl["local"] is not None:
+            L = cl["local"]
+            q = self._contig(self.get(mb, cl["q"], L))
+            k = self._contig(self.get(mb, cl["k"], L))
+            v = self._contig(self.get(mb, cl["v"], L))
+            Bl, Hl = q.shape[0] // s, q.shape[1] // d
+            o = torch.empty(q.shape, dtype=torch.bfloat16, device=self.dev)
+            lse = torch.empty(Bl * Hl, s, dtype=torch.float32, device=self.dev)
+            native.attn_fwd(q, k, v, o, lse, Bl, Hl, s, d, cl["scale"])
+            self.aux.setdefault(mb, {})[cl["S"]] = (o, lse)
+            m = cl["merges"][cl["C"]]
+            if m in self.out_ids:
+                return self._coerce(o, self.graph[m].dims, L, self.spec(m))
+            return o
         rep = replicated(2)
         q = self._contig(self.get(mb, cl["q"], rep))
         k = self._contig(self.get(mb, cl["k"], rep))
@@ -410,28 +483,36 @@ class StageRunner:
         return self._coerce(ctx, self.graph[cl["C"]].dims, replicated(3), self.spec(cl["C"]))
 
     def _run_attn_bwd(self, mb: int, op: _Op):
-        """Fused attention backward.  Key-split: dQ partial sums over the local
-        keys are all-reduced across the key axes; dK / dV come out for the
-        local keys (RRS^A / RS^AR), then reach the nodes' own specs."""
+        """Fused attention backward.  local: dq / dk / dv of the device's tile,
+        written as the head merges' values.  keys: dQ partial sums over the
+        local keys are all-reduced across the key axes; dK / dV come out for
+        the local keys (RRS^A / RS^AR), then reach the nodes' own specs."""
         cl = op.extra
         Bn, H, s, d = cl["heads"]
-        rep = replicated(2)
-        q = self._contig(self.get(mb, cl["q"], rep))
-        k = self._contig(self.get(mb, cl["k"], rep))
-        v = self._contig(self.get(mb, cl["v"], rep))
-        dout = self._contig(self.get(mb, cl["dctx2"], rep))
+        g = self.graph
+        vals = self.vals[mb]
         o, lse = self.aux[mb][cl["S"]]
-        T, hdim = Bn * s, H * d
+        L = cl["local"] if cl["local"] is not None else replicated(2)
+        q = self._contig(self.get(mb, cl["q"], L))
+        k = self._contig(self.get(mb, cl["k"], L))
+        v = self._contig(self.get(mb, cl["v"], L))
+        dout = self._contig(self.get(mb, cl["dctx2"], L))
+        T, hdim = q.shape
+        Bl, Hl = T // s, hdim // d
         k0, k1 = cl["kv"]
-        dvec = torch.empty(Bn * H, s, dtype=torch.float32, device=self.dev)
+        dvec = torch.empty(Bl * Hl, s, dtype=torch.float32, device=self.dev)
         dq_acc = torch.zeros(T, hdim, dtype=torch.float32, device=self.dev)
         dk = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
         dv = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
-        native.attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, Bn, H, s, d, cl["scale"],
+        native.attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, Bl, Hl, s, d, cl["scale"],
                         kv_range=(k0, k1 - k0))
         dq = native.cast_f32_bf16(dq_acc, torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev))
-        g = self.graph
-        vals = self.vals[mb]
+        if cl["local"] is not None:
+            for n, t in ((cl["dqh"], dq), (cl["dkh"], dk), (cl["dvh"], dv)):
+                m = cl["merges"][n]
+                vals[m] = (self._coerce(t, g[m].dims, L, self.spec(m)) if m in self.out_ids
+                           else t)
+            return None
         axes = cl["key_axes"]
         if axes:
             self._allreduce(dq, axes)
@@ -533,7 +614,7 @@ class StageRunner:
 
     def get(self, mb: int, nid: int, req: Spec) -> torch.Tensor:
         """Local shard of node `nid` in layout `req` (reshard on demand)."""
-        have = self.spec(nid)
+        have = self.actual.get(nid) or self.spec(nid)
         v = self.value(mb, nid)
         if req == have:
             return v

@@ -46,5 +46,23 @@ def test_multi_device_parity(plan, n):
     assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
     errs = json.loads(lines[-1])
     assert errs["ok"], errs
-    if "tiny_gpt_tp" in plan:   # GPT-1.3B's (1,2) key-split attention, shrunk
-        assert errs["fused"]["attention_key_split"] > 0, errs
+    if "tiny_gpt_tp" in plan:   # GPT-1.3B's (1,2) stages, shrunk: attention fused
+        assert errs["fused"]["attention"] > 0, errs
+
+
+def test_key_split_attention_parity():
+    """The plan's own key-split attention (scores RRS^1, LSE combine across the
+    axis) forced on the shrunk GPT-1.3B (1,2)-stage plan."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    plan = "plans/tiny_gpt_tp_n4/plan.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", "--master-port", "29477",
+           str(ROOT / "scripts/parity_run.py"), str(ROOT / plan)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "PYTHONPATH": str(ROOT), "MPEXEC_ATTN_KEY_SPLIT": "1"})
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert res.returncode == 0 and lines, res.stdout[-3000:] + res.stderr[-3000:]
+    errs = json.loads(lines[-1])
+    assert errs["ok"], errs
+    assert errs["fused"]["attention_key_split"] > 0, errs
