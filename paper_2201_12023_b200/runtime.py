@@ -231,6 +231,48 @@ class StageRunner:
         self.attn_clusters = self._fuse_attention() if self.fuse_attention else []
         self.fused_epilogues = (self._fuse_epilogues()
                                 if os.environ.get("MPEXEC_FUSE_EPILOGUE", "1") != "0" else 0)
+        self.tok_dw: dict[int, tuple[int, ...]] = {}
+        if os.environ.get("MPEXEC_TOKEN_SPLIT_DW", "1") != "0":
+            self._token_split_dw()
+
+    def have_spec(self, nid: int) -> Spec:
+        """Layout the node's value is actually stored in."""
+        return self.actual.get(nid) or self.spec(nid)
+
+    def _token_split_dw(self) -> None:
+        """dW = transpose(X) @ G with X and G both split over tokens the same
+        way (data parallelism inside the stage): when the plan's algorithm
+        would reshard X or G for it (e.g. a square transpose kept at S^aR, so X
+        must go column-split), compute the local partial X_loc^T G_loc into a
+        full-size fp32 buffer instead and all-reduce it over the token axes
+        once per step (reduce_grads) — the same sum, no per-microbatch
+        traffic.  The skipped transpose is dropped when nothing else reads it."""
+        g = self.graph
+        drop = set()
+        for o in self.bwd_ops:
+            if o.op != "matmul" or not o.grad_direct:
+                continue
+            (a, a_req), (bn, b_req) = o.ins
+            if self.bound[a].op != "transpose" or a not in self.members:
+                continue
+            X = g[a].inputs[0]
+            hx, hb = self.have_spec(X), self.have_spec(bn)
+            if len(hx.dims) != 2 or hx.dims[1] or not hx.dims[0] or hb != hx:
+                continue
+            t_req = canonical(reshape_required(self.bound[a], self.spec(a), 2), self.mesh)
+            costly = False
+            for nid, have, req in ((X, hx, t_req), (a, self.have_spec(a), a_req),
+                                   (bn, hb, b_req)):
+                req = canonical(req, self.mesh)
+                if have != req and self._relayout_plan(tuple(g[nid].dims), have, req)[0] != "local":
+                    costly = True
+            if not costly:
+                continue
+            o.extra = ("tok_dw", X)
+            self.tok_dw[o.nid] = tuple(hx.dims[0])   # full-size buffer: _init_params
+            if all(c == o.nid for c, _ in self.cons[a]) and a not in self.out_ids:
+                drop.add(a)
+        self.bwd_ops = [o for o in self.bwd_ops if o.nid not in drop]
 
     def _fuse_epilogues(self) -> int:
         """Fold a matmul's single trivial consumer into its GEMM epilogue:
@@ -592,7 +634,9 @@ class StageRunner:
             if dw is None:
                 continue
             dws = self.spec(dw)
-            if dws == self.spec(pid):
+            if dw in self.tok_dw:
+                self.gviews[dw] = torch.zeros(g[dw].dims, dtype=torch.float32, device=self.dev)
+            elif dws == self.spec(pid):
                 self.gviews[dw] = self.gradbuf[off:off + math.prod(ld)].view(ld)
             else:
                 dld = local_dims(g[dw].dims, dws, self.mesh)
@@ -721,8 +765,13 @@ class StageRunner:
         raise ExecError(f"gemm operand ranks {a.dim()} / {b.dim()}")
 
     def _run_matmul(self, mb: int, op: _Op) -> Optional[torch.Tensor]:
-        a = self.get(mb, op.ins[0][0], op.ins[0][1])
-        b = self.get(mb, op.ins[1][0], op.ins[1][1])
+        if op.nid in self.tok_dw:
+            X = op.extra[1]
+            a = self.get(mb, X, self.have_spec(X)).transpose(0, 1)
+            b = self.get(mb, op.ins[1][0], self.have_spec(op.ins[1][0]))
+        else:
+            a = self.get(mb, op.ins[0][0], op.ins[0][1])
+            b = self.get(mb, op.ins[1][0], op.ins[1][1])
         a, b = self._gemm_operands(a, b)
         k_axes = op.algo.k_axes
         if op.grad_direct:
@@ -1093,6 +1142,14 @@ class StageRunner:
             if dw is None:
                 continue
             gv = self.gviews[dw]
+            if dw in self.tok_dw:
+                # full partial sums over the local tokens: reduce, keep the param's tile
+                self._allreduce(gv, self.tok_dw[dw])
+                off, ld = self.pviews[pid]
+                box = device_box(g[pid].dims, self.spec(pid), self.mesh, self.me)
+                native.pack_box(gv, tuple(lo for lo, _ in box), tuple(hi - lo for lo, hi in box),
+                                out=self.gradbuf[off:off + math.prod(ld)])
+                continue
             algo = matmul_algo(self.bound[dw].op == "bmm", self.spec(dw), self.mesh)
             if algo.k_axes:
                 self._allreduce(gv, algo.k_axes)
@@ -1244,7 +1301,8 @@ class Executor:
                           fused={"attention": len(r.attn_clusters),
                                  "attention_key_split": sum(1 for c in r.attn_clusters
                                                             if c["key_axes"]),
-                                 "epilogues": r.fused_epilogues})
+                                 "epilogues": r.fused_epilogues,
+                                 "token_split_dw": len(r.tok_dw)})
 
 
 def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, steps: int = 1,
