@@ -419,6 +419,16 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       tma_load_2d(&tmK, kv_full, sK, hh * FA_D, krow0 + kt * FA_BN);
       tma_load_2d(&tmV, kv_full, sV, hh * FA_D, krow0 + kt * FA_BN);
     }
+    // lse / D of the next query tile are prefetched into registers while this
+    // warp waits for a free stage, so their global latency stays off the chain
+    float nl[4], nd[4];
+    const float* lse_row = p.lse + (int64_t)bh * p.s;
+    const float* d_row = p.dvec + (int64_t)bh * p.s;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      nl[k] = lse_row[k * 32 + lane];
+      nd[k] = d_row[k * 32 + lane];
+    }
     for (int i = 0; i < n_q; ++i) {
       const int st = i & 1;
       mbar_wait(&q_empty[st], ((i >> 1) & 1) ^ 1);
@@ -427,14 +437,20 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         tma_load_2d(&tmQ, &q_full[st], sQ + st * FA_TILE, hh * FA_D, row0 + i * FA_BM);
         tma_load_2d(&tmdO, &q_full[st], sdO + st * FA_TILE, hh * FA_D, row0 + i * FA_BM);
       }
-      const int64_t base = (int64_t)bh * p.s + i * FA_BM;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        sts32(smem_u32(sLse + st * 128 + k * 32 + lane),
-              p.lse[base + k * 32 + lane] * 1.4426950408889634f);
-        sts32(smem_u32(sD + st * 128 + k * 32 + lane), p.dvec[base + k * 32 + lane]);
+        sts32(smem_u32(sLse + st * 128 + k * 32 + lane), nl[k] * 1.4426950408889634f);
+        sts32(smem_u32(sD + st * 128 + k * 32 + lane), nd[k]);
       }
       mbar_arrive(&q_full[st]);   // release: publishes the lse / D stores
+      if (i + 1 < n_q) {
+        const int nb = (i + 1) * FA_BM;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          nl[k] = lse_row[nb + k * 32 + lane];
+          nd[k] = d_row[nb + k * 32 + lane];
+        }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {

@@ -64,7 +64,7 @@ def main():
                       "mp_us": t * 1e6}), flush=True)
 
 
-if __name__ == "__main__" and "--attn" not in sys.argv and "--epi" not in sys.argv:
+if __name__ == "__main__" and not {"--attn", "--epi", "--layer"} & set(sys.argv):
     sys.exit(main())
 
 
@@ -107,3 +107,47 @@ def bench_epilogues():
 
 if __name__ == "__main__" and "--epi" in sys.argv:
     bench_epilogues()
+
+
+def bench_layer():
+    """Every GEMM of one GPT-1.3B block for one 8-sequence microbatch, in the
+    form the executor issues it (layouts, fused epilogues, fp32 beta=1 dW)."""
+    T, h, f = 8192, 2048, 8192
+    bf = dict(device="cuda", dtype=torch.bfloat16)
+    X = torch.randn(T, h, **bf)
+    Hh = torch.randn(T, f, **bf)
+    W = torch.randn(h, h, **bf)
+    W1 = torch.randn(h, f, **bf)
+    W2 = torch.randn(f, h, **bf)
+    o_h = torch.empty(T, h, **bf)
+    o_f = torch.empty(T, f, **bf)
+    aux_h = torch.randn(T, h, **bf)
+    aux_f = torch.randn(T, f, **bf)
+    g_hh = torch.zeros(h, h, device="cuda")
+    g_hf = torch.zeros(h, f, device="cuda")
+    g_fh = torch.zeros(f, h, device="cuda")
+    E = native
+    cases = [
+        ("fwd q/k/v/o (x4)", 4, lambda: E.gemm(X, W, o_h), T, h, h),
+        ("fwd fc1 + gelu dual", 1, lambda: E.gemm(X, W1, o_f, epilogue=E.EPI_GELU_DUAL, aux=aux_f), T, f, h),
+        ("fwd fc2 + add", 1, lambda: E.gemm(Hh, W2, o_h, epilogue=E.EPI_ADD, aux=aux_h), T, h, f),
+        ("dX fc2: g W2^T + gelu'", 1, lambda: E.gemm(X, W2.t(), o_f, epilogue=E.EPI_GELU_GRAD, aux=aux_f), T, f, h),
+        ("dX fc1: dH W1^T + add", 1, lambda: E.gemm(Hh, W1.t(), o_h, epilogue=E.EPI_ADD, aux=aux_h), T, h, f),
+        ("dX o/q/k/v: g W^T (+add) (x4)", 4, lambda: E.gemm(X, W.t(), o_h, epilogue=E.EPI_ADD, aux=aux_h), T, h, h),
+        ("dW fc2: a^T g (fp32 +=)", 1, lambda: E.gemm(Hh.t(), X, g_fh, beta=1.0), f, h, T),
+        ("dW fc1: x^T dH (fp32 +=)", 1, lambda: E.gemm(X.t(), Hh, g_hf, beta=1.0), h, f, T),
+        ("dW o/q/k/v: x^T g (fp32 +=) (x4)", 4, lambda: E.gemm(X.t(), X, g_hh, beta=1.0), h, h, T),
+    ]
+    tot_t = tot_f = 0.0
+    for name, n, fn, M, N, K in cases:
+        t = timeit(fn)
+        fl = 2.0 * M * N * K
+        tot_t += n * t
+        tot_f += n * fl
+        print(json.dumps({"gemm": name, "M": M, "N": N, "K": K, "us": t * 1e6,
+                          "tflops": fl / t / 1e12}), flush=True)
+    print(json.dumps({"layer_gemm_ms": tot_t * 1e3, "layer_tflops": tot_f / tot_t / 1e12}), flush=True)
+
+
+if __name__ == "__main__" and "--layer" in sys.argv:
+    bench_layer()
