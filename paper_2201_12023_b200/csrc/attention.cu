@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(192, 2)
 // ------------------------------------------------------------------ backward
 struct FaBwdParams {
   int B, H, s, ld;
-  int kv0;            // first key of the range this grid covers (grid.x key tiles)
+  int kv0;            // first key of the range covered
+  int n_kt;           // key tiles in the range (work tiles = n_kt * B * H)
   float scale;        // 1/sqrt(d)
   const float* lse;   // [B*H, s]
   const float* dvec;  // D = rowsum(dO * O), [B*H, s]
@@ -349,6 +350,13 @@ struct FaBwdParams {
 constexpr int FA_BWD_SMEM = FA_TILE * 14 + 2048 + 256;
 constexpr int FA_BWD_THREADS = 448;   // TMA, MMA, 8 P/dS warps, 4 dQ warps
 
+// Persistent: one CTA per SM walks work tiles w = (bh, key tile) with stride
+// gridDim.x.  Every barrier phase runs on the CTA-global query-tile counter g
+// (tile t, query tile i: g = t * n_q + i), so the pipeline does not drain
+// between work tiles: the next tile's Q/dO loads start as soon as stages free
+// up, its K/V as soon as the last MMA of the previous tile has read K/V
+// (kv_empty), and the dK/dV epilogue of tile t overlaps the K/V load of t+1
+// (the first dV/dK MMA of t+1 waits for acc_free).
 __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -368,24 +376,23 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
   float* sLse = reinterpret_cast<float*>(smem + 14 * FA_TILE);   // [2][128], log2 domain
   float* sD = sLse + 256;                                        // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 14 * FA_TILE + 2048);
-  uint64_t* kv_full = bars;          // K, V
-  uint64_t* q_full = bars + 1;       // [2] Q_i, dO_i
+  uint64_t* kv_full = bars;          // K, V of the work tile
+  uint64_t* q_full = bars + 1;       // [2] Q_g, dO_g (+ lse / D staged)
   uint64_t* q_empty = bars + 3;      // [2]
-  uint64_t* st_full = bars + 5;      // S^T and dP^T of tile i in TMEM
-  uint64_t* ps_full = bars + 6;      // P^T / dS^T of tile i in smem (8 warps)
-  uint64_t* pbuf_free = bars + 7;    // [2] MMAs of a tile done with its P^T / dS^T buffer
+  uint64_t* st_full = bars + 5;      // S^T and dP^T of g in TMEM
+  uint64_t* ps_full = bars + 6;      // P^T / dS^T of g in smem (8 warps)
+  uint64_t* pbuf_free = bars + 7;    // [2] MMAs done with a P^T / dS^T buffer
   uint64_t* dq_full = bars + 9;
   uint64_t* dq_free = bars + 10;     // 4 dQ warps
-  uint64_t* acc_done = bars + 11;
+  uint64_t* acc_done = bars + 11;    // dV / dK of the work tile complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* s_free = bars + 13;      // 8 P/dS warps hold S^T / dP^T of g in registers
+  uint64_t* kv_empty = bars + 14;    // last MMA of the work tile has read K / V
+  uint64_t* acc_free = bars + 15;    // dK / dV TMEM drained by the epilogue (8 warps)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kt = blockIdx.x;      // key tile
-  const int bh = blockIdx.y;
-  const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
   const int n_q = p.s / FA_BM;
-  const int row0 = b * p.s;
-  const int krow0 = row0 + p.kv0;
+  const int n_work = p.n_kt * p.B * p.H;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -403,6 +410,9 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
     mbar_init(acc_done, 1);
+    mbar_init(s_free, 8);
+    mbar_init(kv_empty, 1);
+    mbar_init(acc_free, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -414,42 +424,48 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
                  tdQ = tmem + 384;
 
   if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * FA_TILE);
-      tma_load_2d(&tmK, kv_full, sK, hh * FA_D, krow0 + kt * FA_BN);
-      tma_load_2d(&tmV, kv_full, sV, hh * FA_D, krow0 + kt * FA_BN);
-    }
-    // lse / D of the next query tile are prefetched into registers while this
-    // warp waits for a free stage, so their global latency stays off the chain
+    // TMA producer (lane 0) + lse / D staging (all lanes; the next query tile's
+    // values are prefetched into registers so their latency stays off the chain)
     float nl[4], nd[4];
-    const float* lse_row = p.lse + (int64_t)bh * p.s;
-    const float* d_row = p.dvec + (int64_t)bh * p.s;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      nl[k] = lse_row[k * 32 + lane];
-      nd[k] = d_row[k * 32 + lane];
-    }
-    for (int i = 0; i < n_q; ++i) {
-      const int st = i & 1;
-      mbar_wait(&q_empty[st], ((i >> 1) & 1) ^ 1);
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&q_full[st], 2 * FA_TILE);
-        tma_load_2d(&tmQ, &q_full[st], sQ + st * FA_TILE, hh * FA_D, row0 + i * FA_BM);
-        tma_load_2d(&tmdO, &q_full[st], sdO + st * FA_TILE, hh * FA_D, row0 + i * FA_BM);
-      }
+    auto fetch = [&](int w, int i) {
+      const int bh = w / p.n_kt;
+      const int64_t base = (int64_t)bh * p.s + i * FA_BM;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        sts32(smem_u32(sLse + st * 128 + k * 32 + lane), nl[k] * 1.4426950408889634f);
-        sts32(smem_u32(sD + st * 128 + k * 32 + lane), nd[k]);
+        nl[k] = p.lse[base + k * 32 + lane];
+        nd[k] = p.dvec[base + k * 32 + lane];
       }
-      mbar_arrive(&q_full[st]);   // release: publishes the lse / D stores
-      if (i + 1 < n_q) {
-        const int nb = (i + 1) * FA_BM;
+    };
+    int g = 0, t = 0;
+    if ((int)blockIdx.x < n_work) fetch(blockIdx.x, 0);
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
+      const int bh = w / p.n_kt, kt = w - (w / p.n_kt) * p.n_kt;
+      const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
+      const int row0 = b * p.s;
+      for (int i = 0; i < n_q; ++i, ++g) {
+        const int st = g & 1;
+        mbar_wait(&q_empty[st], ((g >> 1) & 1) ^ 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&q_full[st], 2 * FA_TILE);
+          tma_load_2d(&tmQ, &q_full[st], sQ + st * FA_TILE, hh * FA_D, row0 + i * FA_BM);
+          tma_load_2d(&tmdO, &q_full[st], sdO + st * FA_TILE, hh * FA_D, row0 + i * FA_BM);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          nl[k] = lse_row[nb + k * 32 + lane];
-          nd[k] = d_row[nb + k * 32 + lane];
+          sts32(smem_u32(sLse + st * 128 + k * 32 + lane), nl[k] * 1.4426950408889634f);
+          sts32(smem_u32(sD + st * 128 + k * 32 + lane), nd[k]);
         }
+        mbar_arrive(&q_full[st]);   // release: publishes the lse / D stores
+        if (i == 0) {                // K / V of this tile once the previous tile is done with them
+          if (t > 0) mbar_wait(kv_empty, (t - 1) & 1);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(kv_full, 2 * FA_TILE);
+            tma_load_2d(&tmK, kv_full, sK, hh * FA_D, row0 + p.kv0 + kt * FA_BN);
+            tma_load_2d(&tmV, kv_full, sV, hh * FA_D, row0 + p.kv0 + kt * FA_BN);
+          }
+        }
+        if (i + 1 < n_q) fetch(w, i + 1);
+        else if (w + (int)gridDim.x < n_work) fetch(w + gridDim.x, 0);
       }
     }
   } else if (warp == 1) {
@@ -458,9 +474,13 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       const uint32_t id_acc = umma_idesc_bf16(128, 64, 0, 1);  // P^T/dS^T (K-major) x dO/Q (MN)
       const uint32_t id_dq = umma_idesc_bf16(128, 64, 1, 1);   // dS (MN-major) x K (MN-major)
       const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
-      // dV/dK/dQ of tile j (operands: P^T/dS^T buffer j&1, Q/dO stage j&1)
-      auto issue_acc = [&](int j) {
-        const int bj = j & 1;
+      // dV/dK/dQ of query tile j (global gj) of work tile t
+      auto issue_acc = [&](int j, int gj, int t) {
+        const int bj = gj & 1;
+        if (j == 0 && t > 0) {      // the epilogue of work tile t-1 has drained dK / dV
+          mbar_wait(acc_free, (t - 1) & 1);
+          tc_fence_after();
+        }
         const uint32_t pt = smem_u32(sPt + bj * 2 * FA_TILE), ds = smem_u32(sdSt + bj * 2 * FA_TILE);
         const uint32_t qb = smem_u32(sQ + bj * FA_TILE), dob = smem_u32(sdO + bj * FA_TILE);
 #pragma unroll
@@ -471,7 +491,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
           tc_mma_f16(tdK, umma_desc_sw128(ds + aoff, 16, 1024),
                      umma_desc_sw128(qb + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
         }
-        if (j > 0) mbar_wait(dq_free, (j - 1) & 1);
+        if (gj > 0) mbar_wait(dq_free, (gj - 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < FA_BN / 16; ++kk)
@@ -481,28 +501,36 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         tc_commit(&pbuf_free[bj]);
         tc_commit(&q_empty[bj]);
       };
-      mbar_wait(kv_full, 0);
-      for (int i = 0; i < n_q; ++i) {
-        const int st = i & 1;
-        mbar_wait(&q_full[st], (i >> 1) & 1);
-        if (i > 0) mbar_wait(ps_full, (i - 1) & 1);   // S^T/dP^T(i-1) read, P^T/dS^T(i-1) written
-        tc_fence_after();
-        const uint32_t q_base = smem_u32(sQ + st * FA_TILE);
-        const uint32_t do_base = smem_u32(sdO + st * FA_TILE);
+      int g = 0, t = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
+        mbar_wait(kv_full, t & 1);
+        for (int i = 0; i < n_q; ++i, ++g) {
+          const int st = g & 1;
+          mbar_wait(&q_full[st], (g >> 1) & 1);
+          if (g > 0) mbar_wait(s_free, (g - 1) & 1);    // S^T/dP^T(g-1) in the P warps' registers
+          tc_fence_after();
+          const uint32_t q_base = smem_u32(sQ + st * FA_TILE);
+          const uint32_t do_base = smem_u32(sdO + st * FA_TILE);
 #pragma unroll
-        for (int kk = 0; kk < FA_D / 16; ++kk) {
-          tc_mma_f16(tSt, umma_desc_sw128(k_base + kk * 32, 16, 1024),
-                     umma_desc_sw128(q_base + kk * 32, 16, 1024), id_st, kk > 0);
-          tc_mma_f16(tdPt, umma_desc_sw128(v_base + kk * 32, 16, 1024),
-                     umma_desc_sw128(do_base + kk * 32, 16, 1024), id_st, kk > 0);
+          for (int kk = 0; kk < FA_D / 16; ++kk) {
+            tc_mma_f16(tSt, umma_desc_sw128(k_base + kk * 32, 16, 1024),
+                       umma_desc_sw128(q_base + kk * 32, 16, 1024), id_st, kk > 0);
+            tc_mma_f16(tdPt, umma_desc_sw128(v_base + kk * 32, 16, 1024),
+                       umma_desc_sw128(do_base + kk * 32, 16, 1024), id_st, kk > 0);
+          }
+          tc_commit(st_full);
+          if (i > 0) {
+            mbar_wait(ps_full, (g - 1) & 1);           // P^T/dS^T(g-1) written
+            tc_fence_after();
+            issue_acc(i - 1, g - 1, t);
+          }
         }
-        tc_commit(st_full);
-        if (i > 0) issue_acc(i - 1);
+        mbar_wait(ps_full, (g - 1) & 1);
+        tc_fence_after();
+        issue_acc(n_q - 1, g - 1, t);
+        tc_commit(acc_done);
+        tc_commit(kv_empty);
       }
-      mbar_wait(ps_full, (n_q - 1) & 1);
-      tc_fence_after();
-      issue_acc(n_q - 1);
-      tc_commit(acc_done);
     }
   } else if (warp < 10) {
     // 8 P/dS warps: lane quarter q = warp % 4 selects the TMEM lanes (key rows),
@@ -512,104 +540,134 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     const int r = q * 32 + lane;                        // key row (S^T / dP^T lane)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float sl2 = p.scale * 1.4426950408889634f;
-    for (int i = 0; i < n_q; ++i) {
-      const int bi = i & 1;
-      mbar_wait(&q_full[bi], (i >> 1) & 1);   // lse / D of tile i staged
-      mbar_wait(st_full, i & 1);
-      tc_fence_after();
-      // this P^T / dS^T buffer was last read by the MMAs of tile i-2
-      if (i >= 2) mbar_wait(&pbuf_free[bi], ((i >> 1) & 1) ^ 1);
-      uint8_t* pt = sPt + bi * 2 * FA_TILE;
-      uint8_t* dst = sdSt + bi * 2 * FA_TILE;
-      const uint32_t lse_a = smem_u32(sLse + bi * 128), d_a = smem_u32(sD + bi * 128);
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {          // 16 queries per chunk
-        const int c = half * 4 + cc;
-        uint32_t s16[16], d16[16];
-        tmem_ld16(tSt + lane_off + c * 16, s16);
-        tmem_ld16(tdPt + lane_off + c * 16, d16);
-        float lse2[16], dvv[16];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float4 a = lds128(lse_a + (c * 16 + k * 4) * 4);
-          const float4 bq = lds128(d_a + (c * 16 + k * 4) * 4);
-          lse2[4 * k] = a.x; lse2[4 * k + 1] = a.y; lse2[4 * k + 2] = a.z; lse2[4 * k + 3] = a.w;
-          dvv[4 * k] = bq.x; dvv[4 * k + 1] = bq.y; dvv[4 * k + 2] = bq.z; dvv[4 * k + 3] = bq.w;
-        }
+    int g = 0, t = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
+      for (int i = 0; i < n_q; ++i, ++g) {
+        const int bi = g & 1;
+        mbar_wait(&q_full[bi], (g >> 1) & 1);   // lse / D of g staged
+        mbar_wait(st_full, g & 1);
+        tc_fence_after();
+        // this P^T / dS^T buffer was last read by the MMAs of g-2
+        if (g >= 2) mbar_wait(&pbuf_free[bi], ((g >> 1) & 1) ^ 1);
+        uint8_t* pt = sPt + bi * 2 * FA_TILE;
+        uint8_t* dst = sdSt + bi * 2 * FA_TILE;
+        const uint32_t lse_a = smem_u32(sLse + bi * 128), d_a = smem_u32(sD + bi * 128);
+        // 4 chunks of 16 queries, software-pipelined: the TMEM load of chunk
+        // cc+1 is in flight while chunk cc is computed; once the last chunk is
+        // in registers S^T / dP^T are released (s_free) so the next tile's
+        // S^T / dP^T MMAs overlap this tile's tail
+        uint32_t sa[16], da[16], sb[16], db[16];
+        tmem_ld16(tSt + lane_off + (half * 4) * 16, sa);
+        tmem_ld16(tdPt + lane_off + (half * 4) * 16, da);
         tmem_ld_wait();
-        float pv[16], ds[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          pv[e] = ex2(fmaf(__uint_as_float(s16[e]), sl2, -lse2[e]));
-          ds[e] = pv[e] * (__uint_as_float(d16[e]) - dvv[e]) * p.scale;
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = half * 4 + cc;
+          uint32_t(&s16)[16] = (cc & 1) ? sb : sa;
+          uint32_t(&d16)[16] = (cc & 1) ? db : da;
+          if (cc + 1 < 4) {
+            tmem_ld16(tSt + lane_off + (c + 1) * 16, (cc & 1) ? sa : sb);
+            tmem_ld16(tdPt + lane_off + (c + 1) * 16, (cc & 1) ? da : db);
+          } else {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_free);
+          }
+          float lse2[16], dvv[16];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 a = lds128(lse_a + (c * 16 + k * 4) * 4);
+            const float4 bq = lds128(d_a + (c * 16 + k * 4) * 4);
+            lse2[4 * k] = a.x; lse2[4 * k + 1] = a.y; lse2[4 * k + 2] = a.z; lse2[4 * k + 3] = a.w;
+            dvv[4 * k] = bq.x; dvv[4 * k + 1] = bq.y; dvv[4 * k + 2] = bq.z; dvv[4 * k + 3] = bq.w;
+          }
+          float pv[16], ds[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            pv[e] = ex2(fmaf(__uint_as_float(s16[e]), sl2, -lse2[e]));
+            ds[e] = pv[e] * (__uint_as_float(d16[e]) - dvv[e]) * p.scale;
+          }
+          const int ch = c >> 2, u0 = (c & 3) * 2;
+          st_sw128(pt + ch * FA_TILE, r, u0,
+                   make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]), pack_bf2(pv[4], pv[5]),
+                              pack_bf2(pv[6], pv[7])));
+          st_sw128(pt + ch * FA_TILE, r, u0 + 1,
+                   make_uint4(pack_bf2(pv[8], pv[9]), pack_bf2(pv[10], pv[11]),
+                              pack_bf2(pv[12], pv[13]), pack_bf2(pv[14], pv[15])));
+          st_sw128(dst + ch * FA_TILE, r, u0,
+                   make_uint4(pack_bf2(ds[0], ds[1]), pack_bf2(ds[2], ds[3]), pack_bf2(ds[4], ds[5]),
+                              pack_bf2(ds[6], ds[7])));
+          st_sw128(dst + ch * FA_TILE, r, u0 + 1,
+                   make_uint4(pack_bf2(ds[8], ds[9]), pack_bf2(ds[10], ds[11]),
+                              pack_bf2(ds[12], ds[13]), pack_bf2(ds[14], ds[15])));
+          if (cc + 1 < 4) tmem_ld_wait();
         }
-        const int ch = c >> 2, u0 = (c & 3) * 2;
-        st_sw128(pt + ch * FA_TILE, r, u0,
-                 make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]), pack_bf2(pv[4], pv[5]),
-                            pack_bf2(pv[6], pv[7])));
-        st_sw128(pt + ch * FA_TILE, r, u0 + 1,
-                 make_uint4(pack_bf2(pv[8], pv[9]), pack_bf2(pv[10], pv[11]),
-                            pack_bf2(pv[12], pv[13]), pack_bf2(pv[14], pv[15])));
-        st_sw128(dst + ch * FA_TILE, r, u0,
-                 make_uint4(pack_bf2(ds[0], ds[1]), pack_bf2(ds[2], ds[3]), pack_bf2(ds[4], ds[5]),
-                            pack_bf2(ds[6], ds[7])));
-        st_sw128(dst + ch * FA_TILE, r, u0 + 1,
-                 make_uint4(pack_bf2(ds[8], ds[9]), pack_bf2(ds[10], ds[11]),
-                            pack_bf2(ds[12], ds[13]), pack_bf2(ds[14], ds[15])));
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ps_full);
       }
-      fence_async_smem();
+      // dK (half 0) / dV (half 1) epilogue: key row r
+      const int bh = w / p.n_kt, kt = w - (w / p.n_kt) * p.n_kt;
+      const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
+      mbar_wait(acc_done, t & 1);
+      tc_fence_after();
+      const int64_t grow = (int64_t)b * p.s + p.kv0 + kt * FA_BN + r;
+      const uint32_t tacc = half ? tdV : tdK;
+      uint16_t* out = (half ? p.dV : p.dK) + grow * p.ld + hh * FA_D;
+      uint32_t t16[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tacc + lane_off + c * 16, t16[c]);
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(ps_full);
-    }
-    // dK (half 0) / dV (half 1) epilogue: key row r
-    mbar_wait(acc_done, 0);
-    tc_fence_after();
-    const int64_t grow = krow0 + kt * FA_BN + r;
-    const uint32_t tacc = half ? tdV : tdK;
-    uint16_t* out = (half ? p.dV : p.dK) + grow * p.ld + hh * FA_D;
+      if (lane == 0) mbar_arrive(acc_free);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t t16[16];
-      tmem_ld16(tacc + lane_off + c * 16, t16);
-      tmem_ld_wait();
-      uint4* dstg = reinterpret_cast<uint4*>(out + c * 16);
-      dstg[0] = make_uint4(pack_bf2(__uint_as_float(t16[0]), __uint_as_float(t16[1])),
-                           pack_bf2(__uint_as_float(t16[2]), __uint_as_float(t16[3])),
-                           pack_bf2(__uint_as_float(t16[4]), __uint_as_float(t16[5])),
-                           pack_bf2(__uint_as_float(t16[6]), __uint_as_float(t16[7])));
-      dstg[1] = make_uint4(pack_bf2(__uint_as_float(t16[8]), __uint_as_float(t16[9])),
-                           pack_bf2(__uint_as_float(t16[10]), __uint_as_float(t16[11])),
-                           pack_bf2(__uint_as_float(t16[12]), __uint_as_float(t16[13])),
-                           pack_bf2(__uint_as_float(t16[14]), __uint_as_float(t16[15])));
+      for (int c = 0; c < 4; ++c) {
+        uint4* dstg = reinterpret_cast<uint4*>(out + c * 16);
+        dstg[0] = make_uint4(pack_bf2(__uint_as_float(t16[c][0]), __uint_as_float(t16[c][1])),
+                             pack_bf2(__uint_as_float(t16[c][2]), __uint_as_float(t16[c][3])),
+                             pack_bf2(__uint_as_float(t16[c][4]), __uint_as_float(t16[c][5])),
+                             pack_bf2(__uint_as_float(t16[c][6]), __uint_as_float(t16[c][7])));
+        dstg[1] = make_uint4(pack_bf2(__uint_as_float(t16[c][8]), __uint_as_float(t16[c][9])),
+                             pack_bf2(__uint_as_float(t16[c][10]), __uint_as_float(t16[c][11])),
+                             pack_bf2(__uint_as_float(t16[c][12]), __uint_as_float(t16[c][13])),
+                             pack_bf2(__uint_as_float(t16[c][14]), __uint_as_float(t16[c][15])));
+      }
     }
   } else {
-    // 4 dQ warps: query row r of tile i, fp32 reduction into dQacc
+    // 4 dQ warps: query row r of query tile g, fp32 reduction into dQacc
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    for (int i = 0; i < n_q; ++i) {
-      mbar_wait(dq_full, i & 1);
-      tc_fence_after();
-      float* dq = p.dQacc + (int64_t)(row0 + i * FA_BM + r) * p.ld + hh * FA_D;
+    int g = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const int bh = w / p.n_kt;
+      const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
+      const int row0 = b * p.s;
+      for (int i = 0; i < n_q; ++i, ++g) {
+        mbar_wait(dq_full, g & 1);
+        tc_fence_after();
+        float* dq = p.dQacc + (int64_t)(row0 + i * FA_BM + r) * p.ld + hh * FA_D;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t t16[16];
-        tmem_ld16(tdQ + lane_off + c * 16, t16);
-        tmem_ld_wait();
-        if (c == 3) {   // dQ TMEM fully read: the next dQ MMA may overwrite it
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(dq_free);
-        }
+        for (int c = 0; c < 4; ++c) {
+          uint32_t t16[16];
+          tmem_ld16(tdQ + lane_off + c * 16, t16);
+          tmem_ld_wait();
+          if (c == 3) {   // dQ TMEM fully read: the next dQ MMA may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dq_free);
+          }
 #ifndef MP_FA_NO_DQ_RED
 #pragma unroll
-        for (int e = 0; e < 16; e += 4)
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 16 + e),
-                       "f"(__uint_as_float(t16[e])), "f"(__uint_as_float(t16[e + 1])),
-                       "f"(__uint_as_float(t16[e + 2])), "f"(__uint_as_float(t16[e + 3]))
-                       : "memory");
+          for (int e = 0; e < 16; e += 4)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 16 + e),
+                         "f"(__uint_as_float(t16[e])), "f"(__uint_as_float(t16[e + 1])),
+                         "f"(__uint_as_float(t16[e + 2])), "f"(__uint_as_float(t16[e + 3]))
+                         : "memory");
 #endif
+        }
       }
     }
   }
@@ -792,9 +850,10 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
     cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_BWD_SMEM);
     configured = true;
   }
-  FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, scale, lse, dvec, dq_acc,
-                reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
-  dim3 grid((unsigned)(kv_len / FA_BN), (unsigned)(B * H));
+  FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, (int)(kv_len / FA_BN), scale, lse,
+                dvec, dq_acc, reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
+  const int64_t work = (kv_len / FA_BN) * B * H;
+  dim3 grid((unsigned)(work < num_sms() ? work : num_sms()));
   fa_bwd_kernel<<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, p);
   MP_CHECK_LAUNCH();
   return 0;
