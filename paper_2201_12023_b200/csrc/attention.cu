@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
           tc_mma_f16(tdK, umma_desc_sw128(ds + aoff, 16, 1024),
                      umma_desc_sw128(qb + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
         }
+        tc_commit(&q_empty[bj]);     // Q / dO of gj read: the next load may start
         if (gj > 0) mbar_wait(dq_free, (gj - 1) & 1);
         tc_fence_after();
 #pragma unroll
@@ -499,7 +500,6 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
                      umma_desc_sw128(k_base + kk * 2048, 8192, 1024), id_dq, kk > 0);
         tc_commit(dq_full);
         tc_commit(&pbuf_free[bj]);
-        tc_commit(&q_empty[bj]);
       };
       int g = 0, t = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
