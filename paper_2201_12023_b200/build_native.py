@@ -50,10 +50,14 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+    # experiment hooks: extra -D flags and an alternative output path (the
+    # product library is always built without them)
+    extra = os.environ.get("MPEXEC_NVCC_EXTRA", "").split()
+    out = Path(os.environ.get("MPEXEC_LIB_OUT", LIB))
+    if not force and not extra and out == LIB and not needs_build():
         return LIB
     nccl_lib = NCCL / "lib"
-    cmd = [NVCC, *FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(LIB) + ".tmp",
+    cmd = [NVCC, *FLAGS, *extra, *[str(CSRC / s) for s in SOURCES], "-o", str(out) + ".tmp",
            "-L", str(nccl_lib), "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}", "-lcuda"]
     # libcuda is resolved at run time through cudaGetDriverEntryPoint; link the stub
     # only so the symbol table is complete when a driver is absent (CPU container).
@@ -63,14 +67,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     cmd.remove("-lcuda")
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = (res.stdout or "") + (res.stderr or "")
-    (PKG / "build_native.log").write_text(" ".join(cmd) + "\n" + log)
+    (out.parent / (out.stem + ".build.log")).write_text(" ".join(cmd) + "\n" + log)
     if res.returncode != 0:
         sys.stderr.write(log)
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {PKG / 'build_native.log'}")
-    os.replace(str(LIB) + ".tmp", LIB)
+        raise RuntimeError(f"nvcc failed ({res.returncode}); see {out.parent / (out.stem + ".build.log")}")
+    os.replace(str(out) + ".tmp", out)
     if verbose:
         sys.stdout.write(log)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -66,6 +66,23 @@ __device__ __forceinline__ void tma_load_2d(const void* tmap, uint64_t* bar, voi
       "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// smem -> global element-wise fp32 add of a 2-D box (TMA reduction, L2 does the adds)
+__device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* src, int c0,
+                                                  int c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
+      " [%0, {%2, %3}], [%1];" ::"l"(tmap), "r"(smem_u32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -360,7 +377,7 @@ constexpr int FA_BWD_THREADS = 448;   // TMA, MMA, 8 P/dS warps, 4 dQ warps
 __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                  const FaBwdParams p) {
+                  const __grid_constant__ CUtensorMap tmdQ, const FaBwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) {   // never observed; poison dQ so parity tests catch it
     if (threadIdx.x == 0) p.dQacc[0] = __int_as_float(0x7fc00000);
@@ -381,9 +398,9 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
   uint64_t* q_empty = bars + 3;      // [2]
   uint64_t* st_full = bars + 5;      // S^T and dP^T of g in TMEM
   uint64_t* ps_full = bars + 6;      // P^T / dS^T of g in smem (8 warps)
-  uint64_t* pbuf_free = bars + 7;    // [2] MMAs done with a P^T / dS^T buffer
-  uint64_t* dq_full = bars + 9;
-  uint64_t* dq_free = bars + 10;     // 4 dQ warps
+  uint64_t* pbuf_free = bars + 7;    // [2] P^T / dS^T buffer free (MMAs and dQ reduction done)
+  uint64_t* dq_full = bars + 16;     // [2] dQ of g in TMEM buffer g & 1
+  uint64_t* dq_free = bars + 18;     // [2] 4 dQ warps have read the buffer
   uint64_t* acc_done = bars + 11;    // dV / dK of the work tile complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   uint64_t* s_free = bars + 13;      // 8 P/dS warps hold S^T / dP^T of g in registers
@@ -407,8 +424,10 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     }
     mbar_init(st_full, 1);
     mbar_init(ps_full, 8);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_free, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dq_full[i], 1);
+      mbar_init(&dq_free[i], 4);
+    }
     mbar_init(acc_done, 1);
     mbar_init(s_free, 8);
     mbar_init(kv_empty, 1);
@@ -421,7 +440,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tSt = tmem, tdPt = tmem + 128, tdV = tmem + 256, tdK = tmem + 320,
-                 tdQ = tmem + 384;
+                 tdQ = tmem + 384;   // [2] x 64 columns
 
   if (warp == 0) {
     // TMA producer (lane 0) + lse / D staging (all lanes; the next query tile's
@@ -492,14 +511,13 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
                      umma_desc_sw128(qb + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
         }
         tc_commit(&q_empty[bj]);     // Q / dO of gj read: the next load may start
-        if (gj > 0) mbar_wait(dq_free, (gj - 1) & 1);
+        if (gj >= 2) mbar_wait(&dq_free[bj], ((gj >> 1) & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < FA_BN / 16; ++kk)
-          tc_mma_f16(tdQ, umma_desc_sw128(ds + kk * 2048, FA_TILE, 1024),
+          tc_mma_f16(tdQ + bj * 64, umma_desc_sw128(ds + kk * 2048, FA_TILE, 1024),
                      umma_desc_sw128(k_base + kk * 2048, 8192, 1024), id_dq, kk > 0);
-        tc_commit(dq_full);
-        tc_commit(&pbuf_free[bj]);
+        tc_commit(&dq_full[bj]);   // also: dK / dQ MMAs done with dS^T (the dQ warps reuse it)
       };
       int g = 0, t = 0;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
@@ -584,7 +602,11 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
           float pv[16], ds[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            pv[e] = ex2(fmaf(__uint_as_float(s16[e]), sl2, -lse2[e]));
+  #ifdef MP_FA_EXP_TEST
+          pv[e] = fmaf(__uint_as_float(s16[e]), sl2, -lse2[e]);
+#else
+          pv[e] = ex2(fmaf(__uint_as_float(s16[e]), sl2, -lse2[e]));
+#endif
             ds[e] = pv[e] * (__uint_as_float(d16[e]) - dvv[e]) * p.scale;
           }
           const int ch = c >> 2, u0 = (c & 3) * 2;
@@ -636,40 +658,60 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       }
     }
   } else {
-    // 4 dQ warps: query row r of query tile g, fp32 reduction into dQacc
+    // 4 dQ warps: query row r of query tile g.  dQ(g) leaves TMEM into the
+    // dS^T buffer of g (free once the dQ MMA has read it) as fp32, 128B-swizzled
+    // in two 32-column halves, and is added into dQacc by two TMA bulk
+    // reductions; the buffer is handed back to the P warps once TMA has read it.
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const bool leader = warp == 10 && lane == 0;
     int g = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
       const int bh = w / p.n_kt;
       const int b = bh / p.H, hh = bh - (bh / p.H) * p.H;
       const int row0 = b * p.s;
       for (int i = 0; i < n_q; ++i, ++g) {
-        mbar_wait(dq_full, g & 1);
+        const int bj = g & 1;
+        mbar_wait(&dq_full[bj], (g >> 1) & 1);
         tc_fence_after();
-        float* dq = p.dQacc + (int64_t)(row0 + i * FA_BM + r) * p.ld + hh * FA_D;
+        uint32_t t16[4][16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t t16[16];
-          tmem_ld16(tdQ + lane_off + c * 16, t16);
-          tmem_ld_wait();
-          if (c == 3) {   // dQ TMEM fully read: the next dQ MMA may overwrite it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(dq_free);
-          }
+        for (int c = 0; c < 4; ++c) tmem_ld16(tdQ + bj * 64 + lane_off + c * 16, t16[c]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dq_free[bj]);
 #ifndef MP_FA_NO_DQ_RED
+        uint8_t* stage = sdSt + bj * 2 * FA_TILE;
 #pragma unroll
-          for (int e = 0; e < 16; e += 4)
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 16 + e),
-                         "f"(__uint_as_float(t16[e])), "f"(__uint_as_float(t16[e + 1])),
-                         "f"(__uint_as_float(t16[e + 2])), "f"(__uint_as_float(t16[e + 3]))
+        for (int c = 0; c < 4; ++c) {        // columns 16c .. 16c+15: half c/2, units 4(c&1)..+3
+          uint8_t* chunk = stage + (c >> 1) * FA_TILE;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int u = (c & 1) * 4 + e;
+            const uint32_t a = smem_u32(chunk) + r * 128 + ((u ^ (r & 7)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                         "r"(t16[c][4 * e]), "r"(t16[c][4 * e + 1]), "r"(t16[c][4 * e + 2]),
+                         "r"(t16[c][4 * e + 3])
                          : "memory");
-#endif
+          }
         }
+        fence_async_smem();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (leader) {
+          tma_reduce_add_2d(&tmdQ, stage, hh * FA_D, row0 + i * FA_BM);
+          tma_reduce_add_2d(&tmdQ, stage + FA_TILE, hh * FA_D + 32, row0 + i * FA_BM);
+          bulk_commit();
+          bulk_wait_read0();
+          mbar_arrive(&pbuf_free[bj]);
+        }
+#else
+        if (leader) mbar_arrive(&pbuf_free[bj]);
+#endif
       }
     }
+    if (leader) bulk_wait0();
   }
 
   tc_fence_before();
@@ -772,6 +814,27 @@ static int fa_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ld) {
   return 0;
 }
 
+// (rows x ld) fp32 matrix (dQ accumulator), box 32 cols x 128 rows, 128B swizzle
+static int fa_map_f32(CUtensorMap* m, const void* base, int64_t rows, int64_t ld) {
+  auto enc = fa_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 1;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (f32) failed: " + std::to_string((int)r));
+    return 1;
+  }
+  return 0;
+}
+
 static bool fa_args_ok(const void* p, int64_t ld) {
   return p && (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 8 == 0);
 }
@@ -840,10 +903,11 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
       reinterpret_cast<const uint16_t*>(o), reinterpret_cast<const uint16_t*>(dout), dvec, (int)B,
       (int)H, (int)s, (int)ld);
   MP_CHECK_LAUNCH();
-  CUtensorMap mq, mk, mv, mdo;
+  CUtensorMap mq, mk, mv, mdo, mdq;
   int rc;
   if ((rc = fa_map(&mq, q, B * s, ld)) || (rc = fa_map(&mk, k, B * s, ld)) ||
-      (rc = fa_map(&mv, v, B * s, ld)) || (rc = fa_map(&mdo, dout, B * s, ld)))
+      (rc = fa_map(&mv, v, B * s, ld)) || (rc = fa_map(&mdo, dout, B * s, ld)) ||
+      (rc = fa_map_f32(&mdq, dq_acc, B * s, ld)))
     return rc;
   static bool configured = false;
   if (!configured) {
@@ -854,7 +918,7 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
                 dvec, dq_acc, reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
   const int64_t work = (kv_len / FA_BN) * B * H;
   dim3 grid((unsigned)(work < num_sms() ? work : num_sms()));
-  fa_bwd_kernel<<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, p);
+  fa_bwd_kernel<<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, mdq, p);
   MP_CHECK_LAUNCH();
   return 0;
 }
