@@ -29,6 +29,8 @@ struct GemmParams {
   int nb0, nb1;
   int tiles_m, tiles_n, num_tiles, k_blocks;
   int a_mn, b_mn;
+  int a_mn5, b_mn5;   // MN-major operand staged by one 5-D TMA load per k-block
+  int m_fast;         // tile raster: M index fastest (else N fastest)
   void* C;
   int64_t ldc, c_bs0, c_bs1;
   int c_f32;
@@ -39,6 +41,22 @@ struct GemmParams {
   int n_wide;         // 2-CTA kernel: tiles [0, n_wide) are 256 x BN; the rest are
                       // half-width splits of the last partial wave (wave-quantisation fix)
 };
+
+// tile t -> (batch, m block, n block); the faster index is the one with fewer
+// blocks' worth of reuse to lose (m_fast when N has more tiles than M), so the
+// tiles in flight together share operand blocks in L2
+__device__ __forceinline__ void decode1(const GemmParams& p, int t, int tiles_mn, int& b, int& mb,
+                                        int& nb) {
+  b = t / tiles_mn;
+  const int rem = t - b * tiles_mn;
+  if (p.m_fast) {
+    nb = rem / p.tiles_m;
+    mb = rem - nb * p.tiles_m;
+  } else {
+    mb = rem / p.tiles_n;
+    nb = rem - mb * p.tiles_n;
+  }
+}
 
 template <int BN>
 struct GemmCfg {
@@ -205,10 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int b = t / tiles_mn;
-        const int rem = t - b * tiles_mn;
-        const int mb = rem / p.tiles_n;
-        const int nb = rem - mb * p.tiles_n;
+        int b, mb, nb;
+        decode1(p, t, tiles_mn, b, mb, nb);
         const int b0 = b / p.nb1, b1 = b - (b / p.nb1) * p.nb1;
         const int m0 = mb * BM, n0 = nb * BN;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
@@ -217,14 +233,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
           uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
           const int k0 = kb * BK;
-          if (p.a_mn) {
+          if (p.a_mn5) {
+            tma_load_5d(&tmA, &full[stage], a_dst, 0, k0, m0 / 64, b1, b0);
+          } else if (p.a_mn) {
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i)
               tma_load_4d(&tmA, &full[stage], a_dst + i * 8192, m0 + 64 * i, k0, b1, b0);
           } else {
             tma_load_4d(&tmA, &full[stage], a_dst, k0, m0, b1, b0);
           }
-          if (p.b_mn) {
+          if (p.b_mn5) {
+            tma_load_5d(&tmB, &full[stage], b_dst, 0, k0, n0 / 64, b1, b0);
+          } else if (p.b_mn) {
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i)
               tma_load_4d(&tmB, &full[stage], b_dst + i * 8192, n0 + 64 * i, k0, b1, b0);
@@ -284,10 +304,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const int b = t / tiles_mn;
-      const int rem = t - b * tiles_mn;
-      const int mb = rem / p.tiles_n;
-      const int nb = rem - mb * p.tiles_n;
+      int b, mb, nb;
+      decode1(p, t, tiles_mn, b, mb, nb);
       const int b0 = b / p.nb1, b1 = b - (b / p.nb1) * p.nb1;
       const int64_t row_off = (int64_t)b0 * p.c_bs0 + (int64_t)b1 * p.c_bs1;
       const int m = mb * BM + row;
@@ -363,6 +381,14 @@ __device__ __forceinline__ void tma_load_4d_2sm(const void* tmap, uint32_t bar_c
       "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_2sm(const void* tmap, uint32_t bar_cluster, void* dst,
+                                                int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_f16_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                                uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -395,10 +421,8 @@ __device__ __forceinline__ Tile2 decode2(const GemmParams& p, int t) {
     extra = (u & 1) * (BN / 2);
     narrow = true;
   }
-  const int b = w / tiles_mn;
-  const int rem = w - b * tiles_mn;
-  const int mb = rem / p.tiles_n;
-  const int nb = rem - mb * p.tiles_n;
+  int b, mb, nb;
+  decode1(p, w, tiles_mn, b, mb, nb);
   return Tile2{b / p.nb1, b - (b / p.nb1) * p.nb1, mb, nb * BN + extra, narrow};
 }
 
@@ -468,14 +492,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
           uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
           const int k0 = kb * BK;
-          if (p.a_mn) {
+          if (p.a_mn5) {
+            tma_load_5d_2sm(&tmA, fb, a_dst, 0, k0, m0 / 64, b1, b0);
+          } else if (p.a_mn) {
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i)
               tma_load_4d_2sm(&tmA, fb, a_dst + i * 8192, m0 + 64 * i, k0, b1, b0);
           } else {
             tma_load_4d_2sm(&tmA, fb, a_dst, k0, m0, b1, b0);
           }
-          if (p.b_mn) {
+          if (p.b_mn5) {
+            tma_load_5d_2sm(tl.narrow ? &tmBn : &tmB, fb, b_dst, 0, k0, n0 / 64, b1, b0);
+          } else if (p.b_mn) {
             for (int i = 0; i < nw / 64; ++i)
               tma_load_4d_2sm(&tmB, fb, b_dst + i * 8192, n0 + 64 * i, k0, b1, b0);
           } else {
@@ -620,6 +648,59 @@ static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, 
   return 0;
 }
 
+// rank-5 map of an MN-major operand: {64-element MN chunk, K rows, MN / 64 chunks,
+// nb1, nb0}; box {64, box_k, chunks, 1, 1} lands chunk-major in smem (8 KB per
+// chunk at BK = 64), the layout the MN-major UMMA descriptor expects.
+static int make_map_mn5(CUtensorMap* map, const void* base, int64_t mn, int64_t k, int64_t s1,
+                        int64_t nb1, int64_t bs1, int64_t nb0, int64_t bs0, int box_k,
+                        int chunks) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 1;
+  }
+  const int64_t eb = 2;
+  if (nb1 <= 1) bs1 = s1 * k;
+  if (nb0 <= 1) bs0 = bs1 * (nb1 < 1 ? 1 : nb1);
+  cuuint64_t dims[5] = {64, (cuuint64_t)k, (cuuint64_t)(mn / 64), (cuuint64_t)(nb1 < 1 ? 1 : nb1),
+                        (cuuint64_t)(nb0 < 1 ? 1 : nb0)};
+  cuuint64_t strides[4] = {(cuuint64_t)(s1 * eb), 128, (cuuint64_t)(bs1 * eb),
+                           (cuuint64_t)(bs0 * eb)};
+  for (int i = 0; i < 4; ++i) {
+    if (strides[i] % 16 != 0 || strides[i] == 0) {
+      set_error("gemm operand stride not a multiple of 16 bytes (need 8-element aligned rows)");
+      return 2;
+    }
+  }
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) {
+    set_error("gemm operand base pointer not 16-byte aligned");
+    return 2;
+  }
+  cuuint32_t box[5] = {64, (cuuint32_t)box_k, (cuuint32_t)chunks, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (5-D) failed with code " + std::to_string((int)r));
+    return 1;
+  }
+  return 0;
+}
+
+static bool no_mn5() {
+  static const bool v = getenv("MPEXEC_GEMM_NO_MN5") != nullptr;
+  return v;
+}
+
+static int raster_m_fast(int tiles_m, int tiles_n) {
+  static const char* env = getenv("MPEXEC_GEMM_RASTER");
+  if (env && env[0] == 'n') return 0;
+  if (env && env[0] == 'm') return 1;
+  return tiles_n > tiles_m ? 1 : 0;
+}
+
 template <int BN>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams p,
                        cudaStream_t stream) {
@@ -635,6 +716,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams 
     configured = true;
   }
   p.tiles_n = (p.N + BN - 1) / BN;
+  p.m_fast = raster_m_fast(p.tiles_m, p.tiles_n);
   p.num_tiles = p.tiles_m * p.tiles_n * p.nb0 * p.nb1;
   int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
   gemm_bf16_kernel<BN><<<grid, kThreads, Cfg::SMEM, stream>>>(ma, mb, p);
@@ -658,6 +740,7 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   }
   p.tiles_m = (p.M + 2 * BM - 1) / (2 * BM);
   p.tiles_n = (p.N + BN - 1) / BN;
+  p.m_fast = raster_m_fast(p.tiles_m, p.tiles_n);
   const int wide = p.tiles_m * p.tiles_n * p.nb0 * p.nb1;
   int pairs = num_sms() / 2;
   // Wave quantisation: when the last wave is less than half full, split its
@@ -672,10 +755,6 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   return 0;
 }
 
-static int waves_x1000(int64_t tiles, int slots) {
-  const int64_t w = (tiles + slots - 1) / slots;
-  return (int)(1000 * w * slots / (tiles > 0 ? tiles : 1));
-}
 }  // namespace mp
 
 using namespace mp;
@@ -746,7 +825,9 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
     rc = make_map(&ma, A, K, M, ad[2], nbatch1, ad[5], nbatch0, ad[4], BK, BM);
   } else if (ad[2] == 1) {
     p.a_mn = 1;
-    rc = make_map(&ma, A, M, K, ad[3], nbatch1, ad[5], nbatch0, ad[4], 64, BK);
+    p.a_mn5 = (M % 64 == 0 && !no_mn5()) ? 1 : 0;
+    rc = p.a_mn5 ? make_map_mn5(&ma, A, M, K, ad[3], nbatch1, ad[5], nbatch0, ad[4], BK, BM / 64)
+                 : make_map(&ma, A, M, K, ad[3], nbatch1, ad[5], nbatch0, ad[4], 64, BK);
   } else {
     set_error("mp_gemm_bf16: A needs a unit stride");
     return 2;
@@ -770,8 +851,17 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
   CUtensorMap mbn;
   if (bd[3] == 1) {
     p.b_mn = 1;
-    rc = make_map(&mb, B, N, K, bd[2], nbatch1, bd[5], nbatch0, bd[4], 64, BK);
-    mbn = mb;
+    p.b_mn5 = (N % 64 == 0 && b_box_n % 64 == 0 && !no_mn5()) ? 1 : 0;
+    if (p.b_mn5) {
+      rc = make_map_mn5(&mb, B, N, K, bd[2], nbatch1, bd[5], nbatch0, bd[4], BK, b_box_n / 64);
+      if (!rc && two_sm && b_box_n >= 128)
+        rc = make_map_mn5(&mbn, B, N, K, bd[2], nbatch1, bd[5], nbatch0, bd[4], BK, b_box_n / 128);
+      else
+        mbn = mb;
+    } else {
+      rc = make_map(&mb, B, N, K, bd[2], nbatch1, bd[5], nbatch0, bd[4], 64, BK);
+      mbn = mb;
+    }
   } else if (bd[2] == 1) {
     p.b_mn = 0;
     rc = make_map(&mb, B, K, N, bd[3], nbatch1, bd[5], nbatch0, bd[4], BK, b_box_n);

@@ -2,6 +2,7 @@
 next to torch.matmul (cuBLAS) for context.  CUDA-event timing, warm-up, inputs
 reused (these GEMMs are compute-bound; L2 residency does not change the bound)."""
 import json
+import os
 import sys
 
 import torch
@@ -64,7 +65,7 @@ def main():
                       "mp_us": t * 1e6}), flush=True)
 
 
-if __name__ == "__main__" and not {"--attn", "--epi", "--layer"} & set(sys.argv):
+if __name__ == "__main__" and not {"--attn", "--epi", "--layer", "--one"} & set(sys.argv):
     sys.exit(main())
 
 
@@ -151,3 +152,21 @@ def bench_layer():
 
 if __name__ == "__main__" and "--layer" in sys.argv:
     bench_layer()
+
+
+def bench_one(M, N, K, ta=0, tb=0, iters=5):
+    """One GEMM shape, a few launches (for ncu: -k regex:gemm -s 2 -c 1).
+    ta / tb: operand stored transposed (A MN-major / B K-major)."""
+    a = (torch.randn(K, M, device="cuda", dtype=torch.bfloat16).t() if ta else
+         torch.randn(M, K, device="cuda", dtype=torch.bfloat16))
+    b = (torch.randn(N, K, device="cuda", dtype=torch.bfloat16).t() if tb else
+         torch.randn(K, N, device="cuda", dtype=torch.bfloat16))
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    t = timeit(lambda: native.gemm(a, b, out), iters=iters, warm=2)
+    print(json.dumps({"M": M, "N": N, "K": K, "ta": ta, "tb": tb,
+                      "tflops": 2.0 * M * N * K / t / 1e12, "us": t * 1e6}))
+
+
+if __name__ == "__main__" and "--one" in sys.argv:
+    i = sys.argv.index("--one")
+    bench_one(*(int(x) for x in sys.argv[i + 1:i + 6]), iters=int(os.environ.get("ITERS", "20")))
