@@ -296,7 +296,7 @@ def main():
                          "datasheet_2250": step_flop / t / 1e12 / (2250.0 * args.gpus)},
         "roofline": {"bound": "tensor", "achieved": ach, "peak": sus, "unit": UNIT,
                      "frac": ach / sus, "traffic": None,
-                     "kernel": "mp::gemm_bf16_kernel (tcgen05)",
+                     "kernel": "mp::gemm_bf16_2sm_kernel<256> (tcgen05 cta_group::2)",
                      "launches": g_n, "avg_launch_us": g_time / max(g_n, 1) * 1e6,
                      "achieved_basis": "GEMM FLOPs / union of GEMM launch intervals (CUDA events)",
                      "gemm_share_of_step": g_union / t_local if t_local else None,
