@@ -168,6 +168,10 @@ int mp_comm_destroy(void* comm);
 int mp_allreduce(void* comm, void* buf, int64_t count, int dtype, int op, void* stream);
 int mp_allgather(void* comm, const void* send, void* recv, int64_t sendcount, int dtype,
                  void* stream);
+/* ZeRO realisation of a gradient all-reduce (intra.py:404-424 post_ilp_rewrite):
+ * reduce-scatter of `recvcount * nranks` elements, rank r keeps chunk r. */
+int mp_reduce_scatter(void* comm, const void* send, void* recv, int64_t recvcount, int dtype,
+                      int op, void* stream);
 int mp_group_start(void);
 int mp_group_end(void);
 int mp_send(void* comm, const void* buf, int64_t count, int dtype, int peer, void* stream);

@@ -123,6 +123,10 @@ class Comm:
                         stream=None) -> None:
         native.allgather(group.comm, out_flat, in_flat, stream)
 
+    def reduce_scatter_into(self, out_flat: torch.Tensor, in_flat: torch.Tensor, group: Group,
+                            stream=None) -> None:
+        native.reduce_scatter(group.comm, out_flat, in_flat, stream)
+
     def close(self) -> None:
         for g in self._groups.values():
             if g.comm:

@@ -92,6 +92,17 @@ int mp_allgather(void* comm, const void* send, void* recv, int64_t sendcount, in
   return 0;
 }
 
+int mp_reduce_scatter(void* comm, const void* send, void* recv, int64_t recvcount, int dtype,
+                      int op, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(comm && send && recv && recvcount >= 0, "bad args");
+  if (recvcount == 0) return 0;
+  MP_NCCL(ncclReduceScatter(send, recv, (size_t)recvcount, nccl_dtype(dtype),
+                            op == 1 ? ncclMax : ncclSum, reinterpret_cast<ncclComm_t>(comm),
+                            reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 int mp_group_start(void) {
   clear_error();
   MP_NCCL(ncclGroupStart());

@@ -60,6 +60,7 @@ EXPORTS = {
     "mp_comm_destroy": ([c_vp], c_int),
     "mp_allreduce": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
     "mp_allgather": ([c_vp, c_vp, c_vp, c_i64, c_int, c_vp], c_int),
+    "mp_reduce_scatter": ([c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
     "mp_group_start": ([], c_int),
     "mp_group_end": ([], c_int),
     "mp_send": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
@@ -503,6 +504,21 @@ def allreduce(comm: int, t: torch.Tensor, op: int = 0, stream=None) -> None:
 def allgather(comm: int, out: torch.Tensor, inp: torch.Tensor, stream=None) -> None:
     _check(load().mp_allgather(comm, inp.data_ptr(), out.data_ptr(), inp.numel(), _dt(inp),
                                _stream(stream)), "mp_allgather")
+
+
+def reduce_scatter(comm: int, out: torch.Tensor, inp: torch.Tensor, stream=None) -> None:
+    """Sum-reduce `inp` (nranks * out.numel() elements) across the group; this
+    rank receives its chunk in `out`."""
+    _check(load().mp_reduce_scatter(comm, inp.data_ptr(), out.data_ptr(), out.numel(), _dt(out),
+                                    0, _stream(stream)), "mp_reduce_scatter")
+
+
+def group_start() -> None:
+    _check(load().mp_group_start(), "mp_group_start")
+
+
+def group_end() -> None:
+    _check(load().mp_group_end(), "mp_group_end")
 
 
 def send_recv(comm: int, sends, recvs, stream=None) -> None:

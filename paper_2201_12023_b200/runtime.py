@@ -590,41 +590,101 @@ class StageRunner:
         return self._relayout(self._as3(v), tuple(dims), have, req)
 
     # ------------------------------------------------------------------ params
+    def _zero_axes(self, pid: int) -> tuple[int, ...]:
+        """Axes over which pid's gradient is all-reduced, when the plan's
+        post_ilp_rewrite (intra.py:404-424) realises that all-reduce as
+        reduce-scatter + all-gather: a grad root whose algorithm all-reduces
+        over axes of extent > 1.  Only for gradients laid out like the parameter
+        (or full-size token-split partials) and evenly divisible."""
+        if os.environ.get("MPEXEC_ZERO", "1") == "0":
+            return ()
+        dw = self.grad_nodes.get(pid)
+        if dw is None:
+            return ()
+        if dw in self.tok_dw:
+            axes = self.tok_dw[dw]
+            if not self.spec(pid).is_replicated():
+                return ()
+        else:
+            if self.spec(dw) != self.spec(pid):
+                return ()
+            axes = matmul_algo(self.bound[dw].op == "bmm", self.spec(dw), self.mesh).k_axes
+        gsz = self.mesh.group_extent(axes) if axes else 1
+        if gsz <= 1:
+            return ()
+        n = math.prod(local_dims(self.graph[pid].dims, self.spec(pid), self.mesh))
+        return tuple(axes) if n % gsz == 0 else ()
+
     def _init_params(self, init: Optional[dict[int, np.ndarray]]):
-        """Resident local shards: fp32 master / Adam m, v / fp32 grad in flat
-        buffers (one fused optimizer launch per step) and the bf16 working copy."""
+        """Resident local shards.  bf16 working copies of every parameter live in
+        one flat buffer (wbf16).  fp32 master / Adam m, v live in flat buffers
+        too: full local tiles for plain parameters, and for ZeRO parameters
+        (replicated over the axes their gradient is reduced on) only this
+        device's 1/g chunk — the optimizer state the post_ilp_rewrite shards.
+        Gradients accumulate full-size in gradbuf (the dW GEMMs write there)."""
         g = self.graph
-        sizes = []
+        self.zero: dict[int, tuple[int, ...]] = {}
+        sizes = {}
         for pid in self.param_ids:
-            sizes.append(math.prod(local_dims(g[pid].dims, self.spec(pid), self.mesh)))
-        total = sum(sizes)
+            sizes[pid] = math.prod(local_dims(g[pid].dims, self.spec(pid), self.mesh))
+            ax = self._zero_axes(pid)
+            if ax:
+                self.zero[pid] = ax
+        plain = [p for p in self.param_ids if p not in self.zero]
+        zero = [p for p in self.param_ids if p in self.zero]
+        total = sum(sizes.values())
         self.n_param = total
-        self.master = torch.zeros(total, dtype=torch.float32, device=self.dev)
-        self.m = torch.zeros_like(self.master)
-        self.v = torch.zeros_like(self.master)
-        self.gradbuf = torch.zeros_like(self.master)
         self.wbf16 = torch.zeros(total, dtype=torch.bfloat16, device=self.dev)
+        self.gradbuf = torch.zeros(total, dtype=torch.float32, device=self.dev)
         self.pviews: dict[int, tuple[int, tuple[int, ...]]] = {}
         off = 0
-        for pid, sz in zip(self.param_ids, sizes):
-            ld = local_dims(g[pid].dims, self.spec(pid), self.mesh)
-            self.pviews[pid] = (off, ld)
+        for pid in plain + zero:                  # plain parameters first
+            self.pviews[pid] = (off, tuple(local_dims(g[pid].dims, self.spec(pid), self.mesh)))
+            off += sizes[pid]
+        self.n_plain = sum(sizes[p] for p in plain)
+        # ZeRO chunk of each parameter: (offset in the compact state, chunk, rank in group)
+        self.zchunk: dict[int, tuple[int, int, int]] = {}
+        zoff = 0
+        for pid in zero:
+            grp = self.comm.axis_group(self.st.index, self.mesh, self.zero[pid], self.me)
+            gsz = len(grp.ranks)
+            r = grp.peer(self.me)
+            c = sizes[pid] // gsz
+            self.zchunk[pid] = (zoff, c, r)
+            zoff += c
+        self.n_zero_state = zoff
+        nstate = self.n_plain + zoff
+        self.master = torch.zeros(nstate, dtype=torch.float32, device=self.dev)
+        self.m = torch.zeros_like(self.master)
+        self.v = torch.zeros_like(self.master)
+        self.zgrad = torch.zeros(zoff, dtype=torch.float32, device=self.dev)
+        self.zw = torch.zeros(zoff, dtype=torch.bfloat16, device=self.dev)
+        full_init = torch.zeros(total, dtype=torch.float32, device=self.dev)
+        for pid in self.param_ids:
+            off, ld = self.pviews[pid]
+            sz = sizes[pid]
             box = device_box(g[pid].dims, self.spec(pid), self.mesh, self.me)
             if init is not None:
                 full = np.asarray(init[pid], dtype=np.float32)
                 loc = full[tuple(slice(lo, hi) for lo, hi in box)]
-                self.master[off:off + sz].copy_(torch.from_numpy(np.ascontiguousarray(loc)).reshape(-1))
+                full_init[off:off + sz].copy_(torch.from_numpy(np.ascontiguousarray(loc)).reshape(-1))
             else:
                 gen = torch.Generator(device=self.dev)
                 gen.manual_seed(hash((self.seed, "param", pid)) & 0x7FFFFFFF)
                 # GPT-style init (std 0.02) keeps the 24-block residual stream O(1)
                 full = torch.randn(g[pid].dims, generator=gen, device=self.dev) * self.init_std
                 loc = full[tuple(slice(lo, hi) for lo, hi in box)]
-                self.master[off:off + sz].copy_(loc.reshape(-1))
+                full_init[off:off + sz].copy_(loc.reshape(-1))
                 del full
-            off += sz
         if total:
-            native.cast_f32_bf16(self.master, self.wbf16)
+            native.cast_f32_bf16(full_init, self.wbf16)
+        if self.n_plain:
+            self.master[:self.n_plain].copy_(full_init[:self.n_plain])
+        for pid, (zo, c, r) in self.zchunk.items():
+            off, _ = self.pviews[pid]
+            self.master[self.n_plain + zo:self.n_plain + zo + c].copy_(
+                full_init[off + r * c:off + (r + 1) * c])
+        del full_init
         # gradient buffers of grad_of nodes are laid out in the dW node's own spec;
         # when that differs from the parameter spec a separate fp32 buffer is used.
         self.gviews: dict[int, torch.Tensor] = {}
@@ -634,9 +694,9 @@ class StageRunner:
             if dw is None:
                 continue
             dws = self.spec(dw)
-            if dw in self.tok_dw:
+            if dw in self.tok_dw and pid not in self.zero:
                 self.gviews[dw] = torch.zeros(g[dw].dims, dtype=torch.float32, device=self.dev)
-            elif dws == self.spec(pid):
+            elif dws == self.spec(pid) or dw in self.tok_dw:
                 self.gviews[dw] = self.gradbuf[off:off + math.prod(ld)].view(ld)
             else:
                 dld = local_dims(g[dw].dims, dws, self.mesh)
@@ -1131,15 +1191,29 @@ class StageRunner:
             self.dw_pending = False
 
     def reduce_grads(self):
-        """Finish the gradient of every parameter: all-reduce the k-split partial
-        sums accumulated over the microbatches (sharding.py:284-291; one reduction
-        per step instead of per microbatch, the sum is linear) and move them to
-        the parameter's layout."""
+        """Finish the gradient of every parameter: reduce the k-split partial
+        sums accumulated over the microbatches (sharding.py:284-291; one
+        reduction per step instead of per microbatch, the sum is linear) and
+        move them to the parameter's layout.  Gradient all-reduces the plan
+        rewrites ZeRO-style (intra.py:404-424) become reduce-scatters into this
+        device's optimizer chunk (apply_update all-gathers the new weights)."""
         g = self.graph
         self.join_dw()
+        zs = [pid for pid in self.param_ids if pid in self.zero]
+        if zs:
+            native.group_start()
+            try:
+                for pid in zs:
+                    off, ld = self.pviews[pid]
+                    zo, c, _ = self.zchunk[pid]
+                    grp = self.comm.axis_group(self.st.index, self.mesh, self.zero[pid], self.me)
+                    self.comm.reduce_scatter_into(self.zgrad[zo:zo + c],
+                                                  self.gradbuf[off:off + c * len(grp.ranks)], grp)
+            finally:
+                native.group_end()
         for pid in self.param_ids:
             dw = self.grad_nodes.get(pid)
-            if dw is None:
+            if dw is None or pid in self.zero:
                 continue
             gv = self.gviews[dw]
             if dw in self.tok_dw:
@@ -1160,12 +1234,29 @@ class StageRunner:
                                 out=self.gradbuf[off:off + math.prod(ld)])
 
     def apply_update(self):
+        """Adam on the plain parameters' full tiles and on the ZeRO chunks, then
+        the all-gather half of the rewrite refreshes the replicated bf16 weights."""
         self.step_count += 1
-        if self.n_param:
-            a = self.adam
-            native.adam_step(self.master, self.m, self.v, self.gradbuf, self.wbf16, lr=a.lr,
-                             beta1=a.beta1, beta2=a.beta2, eps=a.eps,
-                             weight_decay=a.weight_decay, grad_scale=1.0, step=self.step_count)
+        if not self.n_param:
+            return
+        a = self.adam
+        kw = dict(lr=a.lr, beta1=a.beta1, beta2=a.beta2, eps=a.eps, weight_decay=a.weight_decay,
+                  grad_scale=1.0, step=self.step_count)
+        n0 = self.n_plain
+        if n0:
+            native.adam_step(self.master[:n0], self.m[:n0], self.v[:n0], self.gradbuf[:n0],
+                             self.wbf16[:n0], **kw)
+        if self.n_zero_state:
+            native.adam_step(self.master[n0:], self.m[n0:], self.v[n0:], self.zgrad, self.zw, **kw)
+            native.group_start()
+            try:
+                for pid, (zo, c, _) in self.zchunk.items():
+                    off, _ = self.pviews[pid]
+                    grp = self.comm.axis_group(self.st.index, self.mesh, self.zero[pid], self.me)
+                    self.comm.all_gather_into(self.wbf16[off:off + c * len(grp.ranks)],
+                                              self.zw[zo:zo + c], grp)
+            finally:
+                native.group_end()
 
     def optimizer_step(self):
         self.reduce_grads()
@@ -1180,7 +1271,14 @@ class StageRunner:
                 gv.zero_()
 
     def local_grad(self, pid: int) -> torch.Tensor:
+        """This device's tile of pid's reduced gradient (after reduce_grads)."""
         off, ld = self.pviews[pid]
+        if pid in self.zero:
+            zo, c, _ = self.zchunk[pid]
+            grp = self.comm.axis_group(self.st.index, self.mesh, self.zero[pid], self.me)
+            full = torch.empty(c * len(grp.ranks), dtype=torch.float32, device=self.dev)
+            self.comm.all_gather_into(full, self.zgrad[zo:zo + c], grp)
+            return full.view(ld)
         return self.gradbuf[off:off + math.prod(ld)].view(ld)
 
     # ------------------------------------------------------------------ step

@@ -21,12 +21,24 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("plan")
     ap.add_argument("--schedule", default="1f1b")
+    ap.add_argument("--train-steps", type=int, default=0,
+                    help="instead of the oracle check: run N steps with Adam updates and "
+                         "print the per-step losses (used to compare optimizer paths)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
         local = int(os.environ.get("LOCAL_RANK", "0"))
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.train_steps:
+        from parity_harness import train_losses
+        losses = train_losses(args.plan, args.schedule, args.train_steps)
+        if losses is not None:
+            print(json.dumps({"losses": losses, "plan": args.plan}), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     from parity_harness import run_plan
     errs = run_plan(args.plan, args.schedule)
     rc = 0

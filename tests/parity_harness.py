@@ -99,3 +99,20 @@ def run_plan(plan_path, schedule="1f1b", seed=0):
     errs["makespan_s"] = res.makespan
     errs["fused"] = res.fused
     return errs
+
+
+def train_losses(plan_path, schedule="1f1b", steps=3, seed=0):
+    """Losses of `steps` training steps (Adam updates between them) on this
+    process group; rank 0 returns them, other ranks None."""
+    import torch.distributed as dist
+    from paper_2201_12023_b200.runtime import Executor
+    doc = json.loads(Path(plan_path).read_text())
+    params, inputs = synth(doc, seed)
+    ex = Executor(doc, schedule=schedule, params=params, inputs=inputs, seed=seed)
+    out = []
+    for _ in range(steps):
+        ex.barrier()
+        ex.step()
+        out.append(ex.loss())
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    return out if rank == 0 else None
