@@ -148,6 +148,21 @@ int mp_attn_combine_finish(void* o, const float* wsum, const float* m, float* ls
                            int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld,
                            void* stream);
 
+/* ---- GShard top-2 routing (MoE builder, paper_2201_12023_b200/builders.py) ---
+ * The MoE graph's gates -> (G, E*C, S) dispatch-mask and gates -> (G, S, E*C)
+ * combine-weight reshapes (graph.py:240-245 layout adapters; the reference has
+ * no MoE builder).  route: int32 [tokens, 4] = {e1, pos1|-1, e2,
+ * pos2|-1} per token, groups of S tokens, capacity C (rule in csrc/moe.cu).
+ * mask mode 0: dispatch ones, mode 1: combine gate weights; `out` is fully
+ * written.  mask_grad (T, E) bf16: mode 1 out[t, e] = d at the routed slot of
+ * (t, e), else 0; mode 0 zeros (the 0/1 dispatch mask has no gradient). */
+int mp_moe_route(const void* gates, int64_t ld, int64_t groups, int S, int E, int C,
+                 int* route, void* stream);
+int mp_moe_mask(const int* route, const void* gates, int64_t ld, void* out, int64_t tokens,
+                int S, int E, int C, int mode, void* stream);
+int mp_moe_mask_grad(const int* route, const void* d, void* out, int64_t tokens, int S, int E,
+                     int C, int mode, void* stream);
+
 /* ---- box pack / unpack (cross-mesh Transfer, reshard.py:32-37,97-108) -----
  * Copies the sub-box [lo, lo+ext) of a strided tensor of rank <= 4 to / from
  * a dense buffer.  dims/strides in elements, elem_bytes in {2,4}. */

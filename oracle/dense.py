@@ -28,6 +28,68 @@ def softmax(x, scale):
     return e / e.sum(axis=-1, keepdims=True)
 
 
+def route(gates, G, S, E, C):
+    """GShard top-2 routing per group of S tokens, capacity C (the rule in the
+    product's csrc/moe.cu header, restated): list of (t, e, slot) kept pairs."""
+    pairs = []
+    g2 = np.asarray(gates, np.float64).reshape(G, S, E)
+    for g in range(G):
+        x = g2[g]
+        e1 = x.argmax(axis=1)                      # first maximum = lowest index
+        x2 = x.copy()
+        x2[np.arange(S), e1] = -np.inf
+        e2 = x2.argmax(axis=1)
+        seen = np.zeros(E, np.int64)
+        pos1 = np.empty(S, np.int64)
+        for s in range(S):
+            pos1[s] = seen[e1[s]]
+            seen[e1[s]] += 1
+        fill = np.minimum(seen, C)
+        for s in range(S):
+            if pos1[s] < C:
+                pairs.append((g * S + s, int(e1[s]), int(pos1[s])))
+        for s in range(S):
+            p = fill[e2[s]]
+            fill[e2[s]] += 1
+            if p < C:
+                pairs.append((g * S + s, int(e2[s]), int(p)))
+    return pairs
+
+
+def pairs_of(route_table):
+    """(T, 4) {e1, pos1|-1, e2, pos2|-1} table (the executor's) -> kept pairs."""
+    r = np.asarray(route_table)
+    return [(t, int(r[t, 2 * k]), int(r[t, 2 * k + 1]))
+            for k in (0, 1) for t in range(r.shape[0]) if r[t, 2 * k + 1] >= 0]
+
+
+def routing_op(code, info, x, gates=None, pairs=None):
+    """pairs: routing decisions to replay instead of deciding from the gates."""
+    if code in ("dispatch", "combine"):
+        G, S, E, C = info
+        out = np.zeros((G, E * C, S) if code == "dispatch" else (G, S, E * C), x.dtype)
+        for t, e, c in (route(x, G, S, E, C) if pairs is None else pairs):
+            g, s = divmod(t, S)
+            if code == "dispatch":
+                out[g, e * C + c, s] = 1.0
+            else:
+                out[g, s, e * C + c] = x[t, e]
+        return out
+    (G, S, E, C), _ = info
+    out = np.zeros((G * S, E), x.dtype)
+    if code == "combine_grad":               # dispatch_grad: the 0/1 mask has none
+        for t, e, c in (route(gates, G, S, E, C) if pairs is None else pairs):
+            g, s = divmod(t, S)
+            out[t, e] = x[g, s, e * C + c]
+    return out
+
+
+def regroup(info, x):
+    A, P, C = info
+    h = x.shape[-1]
+    return x.reshape(A, P, C, h).transpose(1, 0, 2, 3).reshape(P, A * C, h)
+
+
 def reshape_op(code, heads, x):
     if code == "identity":
         return x
@@ -45,8 +107,9 @@ def reshape_op(code, heads, x):
     raise ValueError(code)
 
 
-def eval_node(code, info, n, args, val):
-    """args: input values in slot order; val: all values (for forward refs)."""
+def eval_node(code, info, n, args, val, pairs=None):
+    """args: input values in slot order; val: all values (for forward refs);
+    pairs: replayed MoE routing for routing ops (None: decide from the gates)."""
     if code in ("matmul", "batched_matmul"):
         return args[0] @ args[1]
     if code == "gelu":
@@ -59,6 +122,12 @@ def eval_node(code, info, n, args, val):
         return args[0]
     if code == "gelu_bwd":
         return gelu_grad(val[info]) * args[0]
+    if code in ("dispatch", "combine"):
+        return routing_op(code, info, args[0], pairs=pairs)
+    if code in ("dispatch_grad", "combine_grad"):
+        return routing_op(code, info, args[0], val[info[1]], pairs=pairs)
+    if code == "regroup":
+        return regroup(info, args[0])
     if code == "softmax_bwd":
         y = val[info[0]]
         g = args[0]
@@ -66,8 +135,11 @@ def eval_node(code, info, n, args, val):
     return reshape_op(code, info, args[0])
 
 
-def run(plan_doc, params, inputs, num_microbatches, dtype=np.float64):
-    """-> (loss, grads{param id: array}, outputs{mb: array}) in `dtype`."""
+def run(plan_doc, params, inputs, num_microbatches, dtype=np.float64, trace=None, routes=None):
+    """-> (loss, grads{param id: array}, outputs{mb: array}) in `dtype`.
+    trace: optional {node id: []}; each listed node's value is appended per
+    microbatch.  routes: optional {(microbatch, gates node): (T, 4) table} of
+    MoE routing decisions to replay (the executor's, see ExecResult.routes)."""
     doc, nodes, _ = ir.load(plan_doc)
     bound = ir.bind(nodes)
     grads = {}
@@ -85,7 +157,14 @@ def run(plan_doc, params, inputs, num_microbatches, dtype=np.float64):
                 val[nid] = np.asarray(params[nid], dtype=dtype)
                 continue
             args = [val[p] for p in ir.node_inputs(n)]
-            val[nid] = eval_node(code, info, n, args, val)
+            pairs = None
+            if routes is not None and code in ("dispatch", "combine", "dispatch_grad",
+                                               "combine_grad"):
+                gid = ir.node_inputs(n)[0] if code in ("dispatch", "combine") else info[1]
+                pairs = pairs_of(routes[(mb, gid)])
+            val[nid] = eval_node(code, info, n, args, val, pairs)
+            if trace is not None and nid in trace:
+                trace[nid].append(val[nid])
             if code == "seed":
                 y = val[nid]
                 loss += 0.5 * float((y * y).sum())

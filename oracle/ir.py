@@ -107,7 +107,12 @@ def bind(nodes):
             if co is None:
                 if len(ins) == 2:
                     out[nid] = ("add", None)
-                elif nodes[ins[0]]["kind"] == "batched_matmul":
+                elif any(nodes[c]["kind"] == "reshape" and nodes[c].get("colocate_with") is None
+                         and len(node_dims(nodes[c])) == 3 and len(node_dims(n)) == 2
+                         for c, _ in consumers[nid]):
+                    out[nid] = ("softmax", 1.0)                      # MoE gates
+                elif nodes[ins[0]]["kind"] == "batched_matmul" and \
+                        nodes[nodes[ins[0]]["inputs"][1][0]]["kind"] != "parameter":
                     d = node_dims(nodes[nodes[ins[0]]["inputs"][0][0]])[-1]
                     out[nid] = ("softmax", 1.0 / d ** 0.5)
                 else:
@@ -135,14 +140,25 @@ def bind(nodes):
                 f = nodes[co]
                 if f["kind"] in ("matmul", "batched_matmul"):
                     out[nid] = ("transpose", None)
+                elif out[co][0] in ("dispatch", "combine"):
+                    out[nid] = (out[co][0] + "_grad", (out[co][1], node_inputs(f)[0]))
+                elif out[co][0] == "regroup":
+                    A, P, C = out[co][1]
+                    out[nid] = ("regroup", (P, A, C))
                 else:
                     fc, heads = out[co]
                     inv = {"split": "merge", "split_t": "merge_t", "merge": "split",
                            "merge_t": "split_t", "transpose": "transpose", "identity": "identity"}
                     out[nid] = (inv[fc], heads)
+            elif _routing(nodes, n) is not None:
+                out[nid] = _routing(nodes, n)
+            elif len(src) == 3 and len(dst) == 3 and nodes[ins[0]]["kind"] == "batched_matmul":
+                A, B, _ = src
+                out[nid] = ("regroup", (A, dst[0], B // dst[0]))
             elif len(src) == 2 and len(dst) == 3:
                 tr = any(nodes[c]["kind"] == "batched_matmul" and s == 1
                          and nodes[nodes[c]["inputs"][0][0]]["kind"] == "reshape"
+                         and _routing(nodes, nodes[nodes[c]["inputs"][0][0]]) is None
                          for c, s in consumers[nid])
                 T, h = src
                 X, Y, Z = dst
@@ -159,3 +175,24 @@ def bind(nodes):
         else:
             raise ValueError(f"unsupported kind {k}")
     return out
+
+
+def _routing(nodes, r):
+    """MoE gates (T, E) -> dispatch (G, E*C, S) / combine (G, S, E*C): the
+    product's binding.routing_geom, restated.  info = (G, S, E, C)."""
+    if r["kind"] != "reshape" or r.get("colocate_with") is not None:
+        return None
+    src = nodes[r["inputs"][0][0]]
+    if src["kind"] != "elementwise" or src.get("colocate_with") is not None \
+            or len(src["inputs"]) != 1:
+        return None
+    sd, rd = node_dims(src), node_dims(r)
+    if len(sd) != 2 or len(rd) != 3:
+        return None
+    T, E = sd
+    X, Y, Z = rd
+    if X * Z == T and Y % E == 0:
+        return ("dispatch", (X, Z, E, Y // E))
+    if X * Y == T and Z % E == 0:
+        return ("combine", (X, Y, E, Z // E))
+    raise ValueError(f"reshape of gates {sd} -> {rd}")

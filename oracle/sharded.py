@@ -155,7 +155,11 @@ class ShardedRun:
                 if code in ("identity", "transpose"):
                     self.local[(dev, mb, nid)] = dense.reshape_op(code, info, x)
                 else:
-                    full = dense.reshape_op(code, info, x)
+                    val = {}
+                    if code in ("dispatch_grad", "combine_grad"):
+                        gid = info[1]
+                        val[gid] = self.fetch(st, dev, mb, gid, tuple(() for _ in self.dims(gid)))
+                    full = dense.eval_node(code, info, n, [x], val)
                     box = ir.box_of(dims, out_spec, st.ext, st.coords(dev))
                     self.local[(dev, mb, nid)] = full[ir.sl(box)]
             return
@@ -201,19 +205,20 @@ class ShardedRun:
             trans, gath = xmesh(dims, sspec, src, dspec, st)
             for dev in st.devices:
                 box = ir.box_of(dims, dspec, st.ext, st.coords(dev))
-                self.local[(dev, mb, nid)] = np.full([hi - lo for lo, hi in box], np.nan, self.dtype)
+                self.local[self.key(dev, mb, nid)] = np.full([hi - lo for lo, hi in box], np.nan,
+                                                             self.dtype)
             for s_dev, d_dev, box in trans:
                 sbox = ir.box_of(dims, sspec, src.ext, src.coords(s_dev))
                 dbox = ir.box_of(dims, dspec, st.ext, st.coords(d_dev))
-                self.local[(d_dev, mb, nid)][ir.sl(box, [b[0] for b in dbox])] = \
-                    self.local[(s_dev, mb, nid)][ir.sl(box, [b[0] for b in sbox])]
+                self.local[self.key(d_dev, mb, nid)][ir.sl(box, [b[0] for b in dbox])] = \
+                    self.local[self.key(s_dev, mb, nid)][ir.sl(box, [b[0] for b in sbox])]
             for devs, tile, pieces in gath:
                 for d in devs:
                     for owner, piece in zip(devs, pieces):
                         if owner == d or piece[0][0] >= piece[0][1]:
                             continue
-                        self.local[(d, mb, nid)][ir.sl(piece, [b[0] for b in tile])] = \
-                            self.local[(owner, mb, nid)][ir.sl(piece, [b[0] for b in tile])]
+                        self.local[self.key(d, mb, nid)][ir.sl(piece, [b[0] for b in tile])] = \
+                            self.local[self.key(owner, mb, nid)][ir.sl(piece, [b[0] for b in tile])]
 
     # -------------------------------------------------------------- driver
     def run(self):

@@ -10,8 +10,8 @@ forward (colocate_with is None)
   input            graph input (one synthetic microbatch)
   parameter        weight
   matmul / bmm     y = a @ b                                    (graph.py:187-188)
-  elementwise(a)   softmax(x / sqrt(d)) over the last dim when a is a bmm
-                   output (the attention probabilities, graph.py:300);
+  elementwise(a)   softmax(x / sqrt(d)) over the last dim when a is a bmm of
+                   two activations (the attention probabilities, graph.py:300);
                    tanh-GeLU otherwise (the MLP activation, graph.py:262,308)
   elementwise(a,b) a + b                                        (residual, graph.py:305,311)
   reshape 2D->3D   attention head split (T,h) -> (B*H, s, d); when it feeds the
@@ -19,6 +19,21 @@ forward (colocate_with is None)
                    key-transposed split (B*H, d, s) (graph.py:297-299)
   reshape 3D->2D   head merge (B*H, s, d) -> (T, h)                (graph.py:302)
   reshape reversing dims: transpose; same dims: identity
+  MoE layout adapters (builders.build_moe; no reference builder):
+  elementwise(a) feeding them          softmax over the experts (the gates)
+  reshape gates (T,E) -> (G, E*C, S)   dispatch mask: 1 at each token's routed
+                                       (expert, slot), GShard top-2 routing in
+                                       groups of S tokens, capacity C (csrc/moe.cu)
+  reshape gates (T,E) -> (G, S, E*C)   combine weights: the gate at the same slots
+  reshape of a bmm output, 3D -> 3D    regroup (A, B, h) -> (P, Q, h), C = B/P:
+                                       out[p, a*C + c] = in[a, p*C + c]
+                                       (group-major <-> expert-major, the all-to-all)
+backward of the adapters
+  combine                              (T,E) gradient = the incoming gradient at the
+                                       routed slots (routing is piecewise constant)
+  dispatch                             zero: the 0/1 mask is piecewise constant (the
+                                       bmm producing its input still runs, as planned)
+  regroup                              regroup back
 backward (colocate_with = f)
   elementwise(out), colocated with out       loss seed dL/dy = y   (L = 1/2 |y|^2)
   elementwise(g) colocated with unary f       f'(x) * g (GeLU) / softmax backward
@@ -46,6 +61,10 @@ class Bound:
     # node whose forward tensor the op reads besides its inputs (gelu_bwd / softmax_bwd)
     fwd_ref: Optional[int] = None
     softmax_scale: float = 1.0
+    # MoE routing geometry (G, S, E, C) of dispatch / combine and their gradients
+    route: Optional[tuple[int, int, int, int]] = None
+    # regroup geometry (A, P, C): (A, P*C, h) -> (P, A*C, h)
+    regroup: Optional[tuple[int, int, int]] = None
 
 
 def _head_geom(two_d: tuple[int, int], three_d: tuple[int, int, int],
@@ -75,7 +94,7 @@ def bind(graph: Graph) -> dict[int, Bound]:
         elif n.kind == KIND_RED:
             out[n.id] = Bound("reduce_sum" if fwd else "broadcast")
         elif n.kind == KIND_ELEM:
-            out[n.id] = _bind_elementwise(graph, n, out)
+            out[n.id] = _bind_elementwise(graph, n, out, cons)
         elif n.kind == KIND_RESHAPE:
             out[n.id] = _bind_reshape(graph, n, out, cons)
         else:
@@ -83,11 +102,37 @@ def bind(graph: Graph) -> dict[int, Bound]:
     return out
 
 
-def _bind_elementwise(graph: Graph, n, bound: dict[int, Bound]) -> Bound:
+def routing_geom(graph: Graph, r) -> Optional[tuple[str, tuple[int, int, int, int]]]:
+    """("dispatch" | "combine", (G, S, E, C)) when forward reshape `r` turns MoE
+    gates (a unary forward elementwise of shape (T, E)) into a routing tensor."""
+    if r.kind != KIND_RESHAPE or r.colocate_with is not None:
+        return None
+    src = graph[r.inputs[0]]
+    if src.kind != KIND_ELEM or src.colocate_with is not None or len(src.inputs) != 1:
+        return None
+    if len(src.dims) != 2 or len(r.dims) != 3:
+        return None
+    T, E = src.dims
+    X, Y, Z = r.dims
+    disp = X * Z == T and Y % E == 0
+    comb = X * Y == T and Z % E == 0
+    if disp and comb:
+        raise PlanError(f"node {r.id}: routing reshape {src.dims} -> {r.dims} is ambiguous")
+    if disp:
+        return "dispatch", (X, Z, E, Y // E)
+    if comb:
+        return "combine", (X, Y, E, Z // E)
+    raise PlanError(f"node {r.id}: reshape of gates {src.dims} -> {r.dims} has no binding")
+
+
+def _bind_elementwise(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
     if n.colocate_with is None:
         if len(n.inputs) == 1:
             src = graph[n.inputs[0]]
-            if src.kind == KIND_BMM:
+            if any(graph[c].kind == KIND_RESHAPE and graph[c].colocate_with is None
+                   and len(graph[c].dims) == 3 and len(n.dims) == 2 for c, _ in cons[n.id]):
+                return Bound("softmax", softmax_scale=1.0)       # MoE gates
+            if src.kind == KIND_BMM and graph[src.inputs[1]].kind != KIND_PARAM:
                 d = graph[src.inputs[0]].dims[-1]       # contraction length of q @ k^T
                 return Bound("softmax", softmax_scale=1.0 / float(d) ** 0.5)
             return Bound("gelu")
@@ -120,6 +165,11 @@ def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
             return Bound("transpose")
         if f.kind == KIND_RESHAPE:
             fb = bound[f.id]
+            if fb.op in ("dispatch", "combine"):
+                return Bound(fb.op + "_grad", route=fb.route, fwd_ref=f.inputs[0])
+            if fb.op == "regroup":
+                A, P, C = fb.regroup
+                return Bound("regroup", regroup=(P, A, C))
             inverse = {"split": "merge", "split_t": "merge_t", "merge": "split",
                        "merge_t": "split_t", "transpose": "transpose", "identity": "identity"}
             op = inverse[fb.op]
@@ -127,11 +177,22 @@ def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
         if f.kind == KIND_RED:
             return Bound("broadcast")
         raise PlanError(f"node {n.id}: backward reshape colocated with {f.kind}")
+    rg = routing_geom(graph, n)
+    if rg is not None:
+        return Bound(rg[0], route=rg[1])
+    if len(ind) == 3 and len(outd) == 3 and src.kind == KIND_BMM:
+        A, B, h = ind
+        P, Q, h2 = outd
+        if h != h2 or B % P or Q != A * (B // P):
+            raise PlanError(f"node {n.id}: reshape {ind} -> {outd} is not a regroup")
+        return Bound("regroup", regroup=(A, P, B // P))
     if len(ind) == 2 and len(outd) == 3:
         transposed = False
         for c, slot in cons[n.id]:
             cn = graph[c]
-            if cn.kind == KIND_BMM and slot == 1 and graph[cn.inputs[0]].kind == KIND_RESHAPE:
+            lhs = graph[cn.inputs[0]]
+            if cn.kind == KIND_BMM and slot == 1 and lhs.kind == KIND_RESHAPE and \
+                    routing_geom(graph, lhs) is None:
                 transposed = True
         return Bound("split_t" if transposed else "split",
                      heads=_head_geom(ind, outd, transposed))

@@ -68,6 +68,9 @@ EXPORTS = {
     "mp_ilp_solve": ([c_int, ctypes.POINTER(c_int), c_i64p, c_int, ctypes.POINTER(c_int),
                       ctypes.POINTER(c_int), c_i64p, c_i64, ctypes.POINTER(c_int), c_i64p,
                       ctypes.POINTER(c_int), c_i64p], c_int),
+    "mp_moe_route": ([c_vp, c_i64, c_i64, c_int, c_int, c_int, c_vp, c_vp], c_int),
+    "mp_moe_mask": ([c_vp, c_vp, c_i64, c_vp, c_i64, c_int, c_int, c_int, c_int, c_vp], c_int),
+    "mp_moe_mask_grad": ([c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_int, c_int, c_vp], c_int),
     "mp_pack_box": ([c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp, c_vp], c_int),
     "mp_unpack_box": ([c_vp, c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp], c_int),
     "mp_adam_step": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_f32, c_f32, c_f32, c_f32, c_f32,
@@ -391,6 +394,48 @@ def attn_combine_finish(o, wsum, m, lse, B: int, H: int, s: int, d: int, stream=
 
 
 # --------------------------------------------------------------------------- boxes
+
+# --------------------------------------------------------------------------- MoE routing
+
+def moe_route(gates: torch.Tensor, S: int, C: int, route: Optional[torch.Tensor] = None,
+              stream=None) -> torch.Tensor:
+    """GShard top-2 routing of (T, E) bf16 gates in groups of S tokens, capacity C
+    -> int32 (T, 4) {e1, pos1|-1, e2, pos2|-1} (csrc/moe.cu)."""
+    _require(gates, torch.bfloat16, "gates")
+    T, E = gates.shape
+    if gates.stride(1) != 1 or T % S:
+        raise NativeError("moe_route: gates must be row-major (T, E) with T % S == 0")
+    route = torch.empty(T, 4, dtype=torch.int32, device=gates.device) if route is None else route
+    _check(load().mp_moe_route(gates.data_ptr(), gates.stride(0), T // S, S, E, C,
+                               route.data_ptr(), _stream(stream)), "mp_moe_route")
+    return route
+
+
+def moe_mask(route: torch.Tensor, gates: torch.Tensor, S: int, C: int, mode: int,
+             out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """mode 0: dispatch mask (G, E*C, S); mode 1: combine weights (G, S, E*C)."""
+    _require(gates, torch.bfloat16, "gates")
+    T, E = gates.shape
+    G = T // S
+    shape = (G, E * C, S) if mode == 0 else (G, S, E * C)
+    out = torch.empty(shape, dtype=torch.bfloat16, device=gates.device) if out is None else out
+    _contig(out, "out")
+    _check(load().mp_moe_mask(route.data_ptr(), gates.data_ptr(), gates.stride(0), out.data_ptr(),
+                              T, S, E, C, mode, _stream(stream)), "mp_moe_mask")
+    return out
+
+
+def moe_mask_grad(route: torch.Tensor, d: torch.Tensor, E: int, S: int, C: int, mode: int,
+                  out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """(T, E) bf16: d at each token's routed slots (backward of moe_mask)."""
+    _require(d, torch.bfloat16, "d")
+    _contig(d, "d")
+    T = route.shape[0]
+    out = torch.empty(T, E, dtype=torch.bfloat16, device=d.device) if out is None else out
+    _check(load().mp_moe_mask_grad(route.data_ptr(), d.data_ptr(), out.data_ptr(), T, S, E, C,
+                                   mode, _stream(stream)), "mp_moe_mask_grad")
+    return out
+
 
 def box_view(t: torch.Tensor, lo, ext) -> Optional[torch.Tensor]:
     """Flat zero-copy view of box [lo, lo+ext) when it is one contiguous run of

@@ -34,7 +34,7 @@ from .binding import Bound, bind
 from .comm import Comm
 from .layout import (all_local, allgather_axes, canonical, matmul_algo, relayout_moves,
                      reshape_required)
-from .plan import (ExecPlan, Mesh, PlanError, Spec, box_numel, device_box, load_plan,
+from .plan import (KIND_PARAM, ExecPlan, Mesh, PlanError, Spec, box_numel, device_box, load_plan,
                    local_dims, replicated)
 from .schedule import GPIPE, Instr, Program, build_program
 from .xmesh import recvs_of, sends_of
@@ -67,6 +67,9 @@ class ExecResult:
     outputs: Optional[dict] = None                  # (microbatch, node) -> global forward output
     gpu_launches: int = 0
     fused: dict = field(default_factory=dict)       # this rank's stage: fused clusters / epilogues
+    # MoE routing used (collect=True): (microbatch, gates node) -> int32 (T, 4)
+    # {e1, pos1|-1, e2, pos2|-1}, the decisions the parity check replays
+    routes: Optional[dict] = None
 
 
 @dataclass
@@ -145,6 +148,7 @@ class StageRunner:
         self.aux: dict[int, dict] = {}
         self.loss_acc = torch.zeros(1, dtype=torch.float32, device=self.dev)
         self.outputs: dict[int, torch.Tensor] = {}
+        self.routes: dict[tuple[int, int], np.ndarray] = {}
         self.keep_outputs = False
         self._host_input_bufs: dict = {}
         self.h2d_bytes = 0
@@ -175,11 +179,24 @@ class StageRunner:
         self.bwd_ops: list[_Op] = []
         self.param_ids: list[int] = []
         self.input_ids: list[int] = []
-        for nid in sorted(self.st.op_ids):
+        # Parameters live with their consumers.  The planner's contiguous layer
+        # cut can leave a weight node in one stage and its matmul in the next
+        # (a boundary tensor of the plan); the executor keeps such a weight --
+        # and its fp32 master / Adam state -- in the consuming stage, which also
+        # owns its gradient, and the per-microbatch send/recv of it is elided.
+        self.rehomed = {nid for nid in self.st.input_specs if g[nid].kind == KIND_PARAM}
+        stage_of = self.plan.stage_of_op()
+        for nid in sorted(set(self.st.op_ids) | self.rehomed):
             n = g[nid]
             b = self.bound[nid]
             out = self.spec(nid)
             if b.op == "param":
+                users = {stage_of[c] for c, _ in self.cons[nid]}
+                if len(users) > 1:
+                    raise ExecError(f"parameter {nid} is consumed by stages {sorted(users)}; "
+                                    "a weight shared across stages is not supported")
+                if users and self.st.index not in users:
+                    continue                          # moved to its consuming stage
                 self.param_ids.append(nid)
                 continue
             if b.op == "input":
@@ -198,7 +215,10 @@ class StageRunner:
                     op.grad_direct = True
             elif n.kind == "reshape":
                 req = reshape_required(b, out, len(g[n.inputs[0]].dims))
-                op = _Op(nid, b.op, b, [(n.inputs[0], req)], out)
+                ins = [(n.inputs[0], req)]
+                if b.fwd_ref is not None:          # MoE routing gradients read the gates
+                    ins.append((b.fwd_ref, replicated(len(g[b.fwd_ref].dims))))
+                op = _Op(nid, b.op, b, ins, out)
             elif b.op in ("reduce_sum", "broadcast"):
                 raise ExecError(f"node {nid}: reduction ops are not supported by this executor")
             else:
@@ -899,6 +919,24 @@ class StageRunner:
             y = x
         elif kind == "transpose":
             y = x.transpose(-1, -2)
+        elif kind in ("dispatch", "combine"):
+            G, S, E, C = op.bound.route
+            gates = self._contig(x)
+            route = native.moe_route(gates, S, C)
+            y = native.moe_mask(route, gates, S, C, 0 if kind == "dispatch" else 1)
+            if self.keep_outputs and kind == "dispatch":
+                self.routes[(mb, op.ins[0][0])] = route.cpu().numpy()
+        elif kind in ("dispatch_grad", "combine_grad"):
+            G, S, E, C = op.bound.route
+            gates = self._contig(self.get(mb, op.ins[1][0], op.ins[1][1]))
+            route = native.moe_route(gates, S, C)
+            y = native.moe_mask_grad(route, self._contig(self._as3(x)), E, S, C,
+                                     0 if kind == "dispatch_grad" else 1)
+        elif kind == "regroup":
+            A, P, C = op.bound.regroup
+            x3 = self._as3(x)
+            h = x3.shape[-1]
+            y = self._contig(x3.view(A, P, C, h).permute(1, 0, 2, 3)).view(P, A * C, h)
         else:
             B, H, s, d = op.bound.heads
             if kind == "split":            # (T,h) -> (B,H,s,d)
@@ -1089,6 +1127,9 @@ class StageRunner:
         outs = []
         for bt in bd.tensors:
             node = self.graph[bt.node]
+            if node.kind == KIND_PARAM:               # re-homed weight: resident here
+                outs.append(None)
+                continue
             dspec = canonical(bt.dst_spec, self.mesh)
             shape = local_dims(node.dims, dspec, self.mesh)
             if self.use_graphs:
@@ -1103,6 +1144,8 @@ class StageRunner:
             outs.append((out, _lo(device_box(node.dims, dspec, self.mesh, self.me))))
         recvs = []
         for k, t in recvs_of(bd, self.me):
+            if outs[k] is None:
+                continue
             out, origin = outs[k]
             lo, ext = _lo(_rel(t.box, origin)), _ext(t.box)
             view = native.box_view(out, lo, ext)
@@ -1129,7 +1172,7 @@ class StageRunner:
                 ga = bt.xplan.gathers[k]
                 break
             k -= len(bt.xplan.gathers)
-        if self.me not in ga.devices:
+        if self.me not in ga.devices or self.graph[bt.node].kind == KIND_PARAM:
             return
         out = self.vals[mb][bt.node]
         tile_lo = ga.box[0][0]
@@ -1165,6 +1208,8 @@ class StageRunner:
         for k, t in sends_of(bd, self.me):
             bt = bd.tensors[k]
             node = self.graph[bt.node]
+            if node.kind == KIND_PARAM:               # re-homed to the consumer
+                continue
             v = self._as3(self.value(mb, bt.node))
             mine = _lo(device_box(node.dims, self.spec(bt.node), self.mesh, self.me))
             lo, ext = _lo(_rel(t.box, mine)), _ext(t.box)
@@ -1432,7 +1477,14 @@ def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, s
             if update:
                 ex.runner.apply_update()
     outputs = _collect_outputs(ex.runner, ex.comm, ex.world) if collect else None
-    return ex.result(grads=grads, outputs=outputs, launches=native.launch_count() - launches0)
+    res = ex.result(grads=grads, outputs=outputs, launches=native.launch_count() - launches0)
+    if collect:
+        parts = [ex.runner.routes]
+        if ex.world > 1:
+            parts = [None] * ex.world
+            dist.all_gather_object(parts, ex.runner.routes, group=ex.comm.world_group)
+        res.routes = {k: v for p in parts for k, v in p.items()}
+    return res
 
 
 def _gather_global(runner: StageRunner, comm: Comm, world: int, items: dict) -> dict:

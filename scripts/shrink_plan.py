@@ -26,13 +26,22 @@ def main():
     ap.add_argument("--hidden", type=int, required=True)
     ap.add_argument("--heads", type=int, required=True)
     ap.add_argument("--microbatches", type=int, default=None)
+    ap.add_argument("--builder", choices=("transformer", "moe"), default="transformer")
+    ap.add_argument("--experts", type=int, default=None, help="moe: experts")
+    ap.add_argument("--ffn-mult", type=int, default=8, help="moe: FFN width / hidden")
     a = ap.parse_args()
     sys.path.insert(0, a.reference_src)
     from meshplan import graph as graph_mod
     from meshplan.graph import build_transformer_blocks
     doc = json.loads(Path(a.src).read_text())
-    g = build_transformer_blocks(a.blocks, a.batch, a.seq, a.hidden, a.heads, elem_bytes=2,
-                                 backward=True)
+    if a.builder == "moe":
+        sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+        from paper_2201_12023_b200.builders import build_moe
+        g = build_moe(a.blocks, a.batch, a.seq, a.hidden, a.heads, a.experts,
+                      ffn_mult=a.ffn_mult, elem_bytes=2, backward=True)
+    else:
+        g = build_transformer_blocks(a.blocks, a.batch, a.seq, a.hidden, a.heads, elem_bytes=2,
+                                     backward=True)
     new = json.loads(graph_mod.serialize(g))
     old = doc["graph"]
     if len(new["nodes"]) != len(old["nodes"]):
@@ -45,8 +54,8 @@ def main():
     if a.microbatches:
         doc["num_microbatches"] = a.microbatches
     doc["config"] = dict(doc.get("config", {}), shrunk_from=str(a.src),
-                         dims=dict(blocks=a.blocks, batch=a.batch, seq=a.seq, hidden=a.hidden,
-                                   heads=a.heads))
+                         dims=dict(builder=a.builder, blocks=a.blocks, batch=a.batch, seq=a.seq,
+                                   hidden=a.hidden, heads=a.heads, experts=a.experts))
     Path(a.dst).parent.mkdir(parents=True, exist_ok=True)
     Path(a.dst).write_text(json.dumps(doc, sort_keys=True))
     print("wrote", a.dst)
