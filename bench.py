@@ -136,7 +136,7 @@ def run_reference(args):
             vals.append((v, dt))
     v = statistics.median(x[0] for x in vals)
     dt = statistics.median(x[1] for x in vals)
-    plan_path = Path(args.plan) if args.plan else ROOT / f"plans/gpt13b_n{args.gpus}/plan.json"
+    plan_path = Path(args.plan)
     plan = json.loads(plan_path.read_text())
     step_flop = _plan_flop(plan)
     out = {
@@ -169,11 +169,26 @@ def _rel(p: Path) -> str:
         return str(p)
 
 
+WORKLOADS = {
+    # name: (plan directory prefix, description)
+    "gpt": ("gpt13b", "GPT-3 1.3B (24 blocks, h=2048, 32 heads, seq 1024) fwd+bwd+Adam, "
+                      "Alpa plan for a (1,%d) cluster"),
+    "moe": ("moe24b", "GShard MoE 2.4B (16 layers, h=1024, 16 heads, 16 experts top-2 every 2nd "
+                      "layer, FFN 8h, seq 1024, groups of 1024 tokens, capacity 128) "
+                      "fwd+bwd+Adam, Alpa plan for a (1,%d) cluster (BASELINE configs[2])"),
+}
+
+
+def _workload_of(doc) -> str:
+    return "moe" if any(n["kind"] == "reshape" and len(n["shape"]["dims"]) == 3 and
+                        doc["graph"]["nodes"][n["inputs"][0][0]]["kind"] == "elementwise"
+                        for n in doc["graph"]["nodes"] if "colocate_with" not in n) else "gpt"
+
+
 def _config(n, doc, plan_rel):
     stages = doc["stages"]
     return {
-        "workload": "GPT-3 1.3B (24 blocks, h=2048, 32 heads, seq 1024) fwd+bwd+Adam, "
-                    "Alpa plan for a (1,%d) cluster" % n,
+        "workload": WORKLOADS[_workload_of(doc)][1] % n,
         "global_batch": SEQS_PER_MB * int(doc["num_microbatches"]),
         "seq_len": 1024, "microbatch_seqs": SEQS_PER_MB,
         "microbatches": int(doc["num_microbatches"]),
@@ -194,7 +209,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--plan", default=None)
+    ap.add_argument("--workload", default="gpt", choices=sorted(WORKLOADS),
+                    help="default plan plans/<gpt13b|moe24b>_n<N>/plan.json")
     args = ap.parse_args()
+    if args.plan is None:
+        args.plan = str(ROOT / f"plans/{WORKLOADS[args.workload][0]}_n{args.gpus}/plan.json")
     if args.impl == "reference":
         return run_reference(args)
 
@@ -211,7 +230,7 @@ def main():
     from paper_2201_12023_b200 import native
     from paper_2201_12023_b200.runtime import Executor
 
-    plan_path = Path(args.plan) if args.plan else ROOT / f"plans/gpt13b_n{args.gpus}/plan.json"
+    plan_path = Path(args.plan)
     doc = json.loads(plan_path.read_text())
     step_flop = _plan_flop(doc)
     ex = Executor(doc, schedule="1f1b", seed=1234)
