@@ -205,6 +205,10 @@ int mp_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
 int mp_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream);
 /* y(fp32) += x(bf16)  (gradient accumulation of a bf16 partial). */
 int mp_accum_bf16_f32(const void* x, float* y, int64_t n, void* stream);
+/* Split-K reduction for gradient GEMMs with few output tiles (e.g. the MoE
+ * 1024x1024 attention dW): y = beta*y + sum_p parts[p*n : (p+1)*n], in order. */
+int mp_sum_parts_f32(const float* parts, int64_t nparts, int64_t n, float* y, float beta,
+                     void* stream);
 
 /* ---- planner acceleration --------------------------------
  * Exact branch-and-bound of the intra-op strategy ILP with the reference's

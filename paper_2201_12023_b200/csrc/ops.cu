@@ -428,6 +428,24 @@ __global__ void accum_bf16_f32_kernel(const uint16_t* __restrict__ x, float* __r
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) y[i] += bf2f(x[i]);
 }
 
+// y = beta * y + sum_p parts[p] (split-K partials, summed in fixed order p = 0..)
+__global__ void sum_parts_f32_kernel(const float4* __restrict__ parts, int64_t nparts, int64_t n4,
+                                     float4* __restrict__ y, float beta) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (beta != 0.f) {
+      float4 v = y[i];
+      acc = make_float4(beta * v.x, beta * v.y, beta * v.z, beta * v.w);
+    }
+    for (int64_t p = 0; p < nparts; ++p) {
+      float4 v = __ldcs(parts + p * n4 + i);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    y[i] = acc;
+  }
+}
+
 }  // namespace mp
 
 using namespace mp;
@@ -609,6 +627,20 @@ int mp_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream) {
   MP_CHECK_ARG(x && y && n >= 0, "bad args");
   if (n == 0) return 0;
   cast_bf16_f32_kernel<<<grid_for(n, 256), 256, 0, MP_STREAM(stream)>>>((const uint16_t*)x, y, n);
+  MP_CHECK_LAUNCH();
+  return 0;
+}
+
+int mp_sum_parts_f32(const float* parts, int64_t nparts, int64_t n, float* y, float beta,
+                     void* stream) {
+  clear_error();
+  MP_CHECK_ARG(parts && y && nparts >= 1 && n >= 0 && n % 4 == 0 &&
+                   reinterpret_cast<uintptr_t>(parts) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(y) % 16 == 0,
+               "bad args (16-byte aligned, n % 4 == 0)");
+  if (n == 0) return 0;
+  sum_parts_f32_kernel<<<grid_for(n / 4, 256), 256, 0, MP_STREAM(stream)>>>(
+      (const float4*)parts, nparts, n / 4, (float4*)y, beta);
   MP_CHECK_LAUNCH();
   return 0;
 }

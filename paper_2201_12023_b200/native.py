@@ -78,6 +78,7 @@ EXPORTS = {
     "mp_cast_f32_bf16": ([c_vp, c_vp, c_i64, c_vp], c_int),
     "mp_cast_bf16_f32": ([c_vp, c_vp, c_i64, c_vp], c_int),
     "mp_accum_bf16_f32": ([c_vp, c_vp, c_i64, c_vp], c_int),
+    "mp_sum_parts_f32": ([c_vp, c_i64, c_i64, c_vp, c_f32, c_vp], c_int),
 }
 
 
@@ -190,6 +191,11 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
         if xb != cb or xd[0] != cd[0] or xd[1] != cd[1] or xd[3] != 1:
             raise NativeError("aux must match out's shape with unit column stride")
         aux_ptr, aux_desc = aux.data_ptr(), _arr([xd[2], xd[4], xd[5]])
+    if epi == 0 and beta != 0.0 and out.dtype == torch.float32 and a.dim() == 2 and \
+            b.dim() == 2 and out.is_contiguous():
+        s = _split_k(ad[0], bd[1], ad[1])
+        if s > 1:
+            return _gemm_split_k(a, b, out, s, alpha, beta, stream)
     st = _stream(stream)
     timer = gemm_timer
     if timer is not None:
@@ -203,6 +209,44 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
     if timer is not None:
         e1.record()
         timer.append((2.0 * ad[0] * ad[1] * bd[1] * ab[0] * ab[1], e0, e1))
+    return out
+
+
+SPLIT_K = os.environ.get("MPEXEC_SPLIT_K", "1") != "0"
+
+
+def _split_k(M: int, N: int, K: int) -> int:
+    """K splits for an accumulating fp32 GEMM whose output tiles fill at most half
+    the machine (2-CTA pair tiles on 74 SM pairs, else 1-CTA tiles on 148 SMs):
+    the largest power of two keeping tiles * splits within one wave and
+    K / splits >= 512 in whole 64-deep k-blocks."""
+    if not SPLIT_K:
+        return 1
+    if M >= 256 and N >= 256:
+        tiles, cap = -(-M // 256) * -(-N // 256), 74
+    else:
+        bn = 256 if N > 128 else (128 if N > 64 else 64)
+        tiles, cap = -(-M // 128) * -(-N // bn), 148
+    s = 1
+    while tiles * s * 2 <= cap and K % (64 * s * 2) == 0 and K // (s * 2) >= 512:
+        s *= 2
+    return s
+
+
+def _gemm_split_k(a, b, out, s, alpha, beta, stream):
+    """out = beta*out + alpha*a@b as s K-chunk GEMMs (one batched launch into fp32
+    partials) plus an in-order sum (deterministic)."""
+    M, K = a.shape
+    N = b.shape[1]
+    kc = K // s
+    a3 = a.as_strided((s, M, kc), (kc * a.stride(1), a.stride(0), a.stride(1)))
+    b3 = b.as_strided((s, kc, N), (kc * b.stride(0), b.stride(0), b.stride(1)))
+    parts = torch.empty(s, M, N, dtype=torch.float32, device=out.device)
+    gemm(a3, b3, parts, alpha=alpha, beta=0.0, stream=stream)
+    _check(load().mp_sum_parts_f32(parts.data_ptr(), s, M * N, out.data_ptr(), float(beta),
+                                   _stream(stream)), "mp_sum_parts_f32")
+    if stream is not None:
+        parts.record_stream(stream)
     return out
 
 

@@ -81,6 +81,9 @@ class AdamConfig:
     weight_decay: float = 0.0
 
 
+FUSE_BMM_EPI = os.environ.get("MPEXEC_FUSE_BMM_EPILOGUE", "1") == "1"
+
+
 def _lo(box):
     return tuple(lo for lo, _ in box)
 
@@ -307,7 +310,8 @@ class StageRunner:
             pos = {o.nid: i for i, o in enumerate(ops)}
             removed = set()
             for i, o in enumerate(ops):
-                if o.op != "matmul" or o.grad_direct or o.algo.k_axes or o.epi is not None \
+                if o.op not in ("matmul", "bmm") or o.grad_direct or o.algo.k_axes \
+                        or o.epi is not None or o.extra is not None \
                         or o.nid in self.st.output_specs:
                     continue
                 users = self.cons[o.nid]
@@ -316,6 +320,10 @@ class StageRunner:
                 u = users[0][0]
                 uop = ops[pos[u]]
                 if self.spec(u) != o.out_spec:
+                    continue
+                # bmm: the MoE expert FFN only (GPU time at K = 1024, graph-timed:
+                # dual 306 us vs 227 + 87 us unfused; GeLU' 370 vs 227 + 174 us)
+                if o.op == "bmm" and (uop.op not in ("gelu", "gelu_bwd") or not FUSE_BMM_EPI):
                     continue
                 if uop.op == "gelu":
                     o.epi = ("dual", u, None)

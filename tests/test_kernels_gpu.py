@@ -201,3 +201,25 @@ def test_gemm_fused_epilogues(M, N, K):
     native.gemm(a, b, out, epilogue=native.EPI_GELU_DUAL, aux=act)
     assert rel_err(out, acc) < 1e-2
     assert rel_err(act, torch.nn.functional.gelu(acc, approximate="tanh")) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K,ta", [(1024, 1024, 8192, 1), (1024, 16, 8192, 1), (512, 512, 4096, 0)])
+def test_gemm_split_k_accumulate(M, N, K, ta):
+    """Few-tile fp32 += GEMMs (MoE attention / gating dW) take the split-K path:
+    one batched launch into partials + an in-order sum; same result as the
+    unsplit kernel to fp32 rounding, 2e-3 against torch fp32."""
+    assert native._split_k(M, N, K) > 1
+    a = rnd(K, M).t() if ta else rnd(M, K)
+    b = rnd(K, N)
+    base = torch.randn(M, N, device="cuda")
+    out = base.clone()
+    native.gemm(a, b, out, beta=1.0)
+    native.SPLIT_K = False
+    try:
+        ref1 = base.clone()
+        native.gemm(a, b, ref1, beta=1.0)
+    finally:
+        native.SPLIT_K = True
+    ref = base + a.float() @ b.float()
+    assert rel_err(out, ref) < 2e-3
+    assert rel_err(out, ref1) < 1e-5
