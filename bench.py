@@ -176,10 +176,16 @@ WORKLOADS = {
     "moe": ("moe24b", "GShard MoE 2.4B (16 layers, h=1024, 16 heads, 16 experts top-2 every 2nd "
                       "layer, FFN 8h, seq 1024, groups of 1024 tokens, capacity 128) "
                       "fwd+bwd+Adam, Alpa plan for a (1,%d) cluster (BASELINE configs[2])"),
+    "wresnet": ("wresnet1b", "Wide-ResNet-50 (base 320, width 2, 1.68e9 params, 224x224, 1024 "
+                             "classes; convs as im2col + tcgen05 GEMM) fwd+bwd+Adam, 32 images "
+                             "per microbatch, 48 microbatches, Alpa plan for a (1,%d) cluster "
+                             "(BASELINE configs[3])"),
 }
 
 
 def _workload_of(doc) -> str:
+    if any(n["kind"].startswith("reduction") for n in doc["graph"]["nodes"]):
+        return "wresnet"
     return "moe" if any(n["kind"] == "reshape" and len(n["shape"]["dims"]) == 3 and
                         doc["graph"]["nodes"][n["inputs"][0][0]]["kind"] == "elementwise"
                         for n in doc["graph"]["nodes"] if "colocate_with" not in n) else "gpt"
@@ -187,10 +193,18 @@ def _workload_of(doc) -> str:
 
 def _config(n, doc, plan_rel):
     stages = doc["stages"]
+    wl = _workload_of(doc)
+    if wl == "wresnet":
+        imgs = next(doc["graph"]["nodes"][n["inputs"][0][0]]["shape"]["dims"][0]
+                    for n in doc["graph"]["nodes"] if n["kind"].startswith("reduction"))
+        batch = {"global_batch": imgs * int(doc["num_microbatches"]), "image": 224,
+                 "microbatch_images": imgs}
+    else:
+        batch = {"global_batch": SEQS_PER_MB * int(doc["num_microbatches"]), "seq_len": 1024,
+                 "microbatch_seqs": SEQS_PER_MB}
     return {
-        "workload": WORKLOADS[_workload_of(doc)][1] % n,
-        "global_batch": SEQS_PER_MB * int(doc["num_microbatches"]),
-        "seq_len": 1024, "microbatch_seqs": SEQS_PER_MB,
+        "workload": WORKLOADS[wl][1] % n,
+        **batch,
         "microbatches": int(doc["num_microbatches"]),
         "plan": plan_rel,
         "parallelism": "+".join(f"stage{s['index']}:{s['logical_view'][0]}x{s['logical_view'][1]}"

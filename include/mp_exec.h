@@ -163,6 +163,20 @@ int mp_moe_mask(const int* route, const void* gates, int64_t ld, void* out, int6
 int mp_moe_mask_grad(const int* route, const void* d, void* out, int64_t tokens, int S, int E,
                      int C, int mode, void* stream);
 
+/* ---- Wide-ResNet layout adapters (builders.build_wide_resnet; the IR has no
+ * convolution): NHWC activations (rows (n, y, x), columns c), bf16.
+ * im2col: k x k (odd) window, stride s, zero padding k/2 -> rows (n, oy, ox),
+ * columns (ky, kx, c); backward=1 is its adjoint col2im (x = d columns,
+ * out = (N*H*W, C)).  subsample: out = in at (oy*s, ox*s); backward scatters into
+ * zeros.  reduce_mid: (A, B, C) -> (A, C) sum over B (the head's pooling
+ * reduction, graph.py:232-237); broadcast=1 its backward (A, C) -> (A, B, C). */
+int mp_im2col(const void* x, void* out, int64_t N, int64_t H, int64_t W, int64_t C, int k,
+              int s, int backward, void* stream);
+int mp_subsample(const void* x, void* out, int64_t N, int64_t H, int64_t W, int64_t C, int s,
+                 int backward, void* stream);
+int mp_reduce_mid(const void* x, void* out, int64_t A, int64_t B, int64_t C, int broadcast,
+                  void* stream);
+
 /* ---- box pack / unpack (cross-mesh Transfer, reshard.py:32-37,97-108) -----
  * Copies the sub-box [lo, lo+ext) of a strided tensor of rank <= 4 to / from
  * a dense buffer.  dims/strides in elements, elem_bytes in {2,4}. */

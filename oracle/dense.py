@@ -90,6 +90,34 @@ def regroup(info, x):
     return x.reshape(A, P, C, h).transpose(1, 0, 2, 3).reshape(P, A * C, h)
 
 
+def conv_op(code, info, x):
+    """Wide-ResNet adapters on NHWC rows (restating csrc/conv.cu's contract)."""
+    N, H, W, C, k, s = info
+    p = k // 2
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    if code == "subsample":
+        return x.reshape(N, H, W, C)[:, ::s, ::s][:, :Ho, :Wo].reshape(N * Ho * Wo, C)
+    if code == "subsample_grad":
+        out = np.zeros((N, H, W, C), x.dtype)
+        out[:, ::s, ::s][:, :Ho, :Wo] = x.reshape(N, Ho, Wo, C)
+        return out.reshape(N * H * W, C)
+    if code == "im2col":
+        xp = np.zeros((N, H + 2 * p, W + 2 * p, C), x.dtype)
+        xp[:, p:p + H, p:p + W] = x.reshape(N, H, W, C)
+        cols = np.empty((N, Ho, Wo, k, k, C), x.dtype)
+        for ky in range(k):
+            for kx in range(k):
+                cols[:, :, :, ky, kx] = xp[:, ky:ky + s * Ho:s, kx:kx + s * Wo:s]
+        return cols.reshape(N * Ho * Wo, k * k * C)
+    # col2im: the adjoint of im2col
+    d = x.reshape(N, Ho, Wo, k, k, C)
+    xp = np.zeros((N, H + 2 * p, W + 2 * p, C), x.dtype)
+    for ky in range(k):
+        for kx in range(k):
+            xp[:, ky:ky + s * Ho:s, kx:kx + s * Wo:s] += d[:, :, :, ky, kx]
+    return xp[:, p:p + H, p:p + W].reshape(N * H * W, C)
+
+
 def reshape_op(code, heads, x):
     if code == "identity":
         return x
@@ -128,6 +156,13 @@ def eval_node(code, info, n, args, val, pairs=None):
         return routing_op(code, info, args[0], val[info[1]], pairs=pairs)
     if code == "regroup":
         return regroup(info, args[0])
+    if code in ("im2col", "col2im", "subsample", "subsample_grad"):
+        return conv_op(code, info, args[0])
+    if code == "reduce_sum":
+        return args[0].sum(axis=info)
+    if code == "broadcast":
+        shape = tuple(n["shape"]["dims"])
+        return np.broadcast_to(np.expand_dims(args[0], 1), shape).copy()
     if code == "softmax_bwd":
         y = val[info[0]]
         g = args[0]

@@ -91,6 +91,32 @@ def node_inputs(n):
 
 
 # ----------------------------------------------------------------- binding
+def _batch(nodes):
+    """images per microbatch: leading dim of the pooling reduction's (N, HW, C) input"""
+    for n in nodes:
+        if n["kind"].startswith("reduction") and n.get("colocate_with") is None:
+            d = node_dims(nodes[n["inputs"][0][0]])
+            if len(d) == 3:
+                return d[0]
+    return None
+
+
+def _conv(src, dst, batch):
+    """NHWC im2col (k x k, stride s, pad k/2) or subsample reshape -> (code, (N,H,W,C,k,s))"""
+    if batch is None:
+        return None
+    (ri, ci), (ro, co) = src, dst
+    H = int(round((ri / batch) ** 0.5))
+    Ho = int(round((ro / batch) ** 0.5))
+    k = int(round((co / ci) ** 0.5))
+    if batch * H * H != ri or batch * Ho * Ho != ro or k * k * ci != co or k % 2 == 0:
+        return None
+    s = max(1, H // Ho)
+    if (H + 2 * (k // 2) - k) // s + 1 != Ho:
+        return None
+    return ("im2col" if k > 1 else "subsample", (batch, H, H, ci, k, s))
+
+
 def bind(nodes):
     """node id -> (code, info).  Same rules as the product's binding, restated."""
     out = {}
@@ -98,17 +124,19 @@ def bind(nodes):
     for n in nodes:
         for s, (p, _) in enumerate(n["inputs"]):
             consumers[p].append((n["id"], s))
+    batch = _batch(nodes)
     for n in nodes:
         k, nid, ins = n["kind"], n["id"], node_inputs(n)
         co = n.get("colocate_with")
         if k in ("input", "parameter", "matmul", "batched_matmul"):
             out[nid] = (k, None)
+        elif k.startswith("reduction"):
+            out[nid] = ("reduce_sum", int(k.split(":")[1]))
         elif k == "elementwise":
             if co is None:
                 if len(ins) == 2:
                     out[nid] = ("add", None)
-                elif any(nodes[c]["kind"] == "reshape" and nodes[c].get("colocate_with") is None
-                         and len(node_dims(nodes[c])) == 3 and len(node_dims(n)) == 2
+                elif any(_routing(nodes, nodes[c], consumers) is not None
                          for c, _ in consumers[nid]):
                     out[nid] = ("softmax", 1.0)                      # MoE gates
                 elif nodes[ins[0]]["kind"] == "batched_matmul" and \
@@ -140,6 +168,11 @@ def bind(nodes):
                 f = nodes[co]
                 if f["kind"] in ("matmul", "batched_matmul"):
                     out[nid] = ("transpose", None)
+                elif f["kind"].startswith("reduction"):
+                    out[nid] = ("broadcast", None)
+                elif out[co][0] in ("im2col", "subsample"):
+                    out[nid] = ("col2im" if out[co][0] == "im2col" else "subsample_grad",
+                                out[co][1])
                 elif out[co][0] in ("dispatch", "combine"):
                     out[nid] = (out[co][0] + "_grad", (out[co][1], node_inputs(f)[0]))
                 elif out[co][0] == "regroup":
@@ -150,15 +183,15 @@ def bind(nodes):
                     inv = {"split": "merge", "split_t": "merge_t", "merge": "split",
                            "merge_t": "split_t", "transpose": "transpose", "identity": "identity"}
                     out[nid] = (inv[fc], heads)
-            elif _routing(nodes, n) is not None:
-                out[nid] = _routing(nodes, n)
+            elif _routing(nodes, n, consumers) is not None:
+                out[nid] = _routing(nodes, n, consumers)
             elif len(src) == 3 and len(dst) == 3 and nodes[ins[0]]["kind"] == "batched_matmul":
                 A, B, _ = src
                 out[nid] = ("regroup", (A, dst[0], B // dst[0]))
             elif len(src) == 2 and len(dst) == 3:
                 tr = any(nodes[c]["kind"] == "batched_matmul" and s == 1
                          and nodes[nodes[c]["inputs"][0][0]]["kind"] == "reshape"
-                         and _routing(nodes, nodes[nodes[c]["inputs"][0][0]]) is None
+                         and _routing(nodes, nodes[nodes[c]["inputs"][0][0]], consumers) is None
                          for c, s in consumers[nid])
                 T, h = src
                 X, Y, Z = dst
@@ -170,14 +203,19 @@ def bind(nodes):
                 out[nid] = ("merge", (T // seq, h // d, seq, d))
             elif src == dst:
                 out[nid] = ("identity", None)
-            else:
+            elif src[::-1] == dst:
                 out[nid] = ("transpose", None)
+            else:
+                cv = _conv(src, dst, batch)
+                if cv is None:
+                    raise ValueError(f"reshape {src} -> {dst}")
+                out[nid] = cv
         else:
             raise ValueError(f"unsupported kind {k}")
     return out
 
 
-def _routing(nodes, r):
+def _routing(nodes, r, consumers):
     """MoE gates (T, E) -> dispatch (G, E*C, S) / combine (G, S, E*C): the
     product's binding.routing_geom, restated.  info = (G, S, E, C)."""
     if r["kind"] != "reshape" or r.get("colocate_with") is not None:
@@ -188,6 +226,8 @@ def _routing(nodes, r):
         return None
     sd, rd = node_dims(src), node_dims(r)
     if len(sd) != 2 or len(rd) != 3:
+        return None
+    if not any(nodes[c]["kind"] == "batched_matmul" and s == 0 for c, s in consumers[r["id"]]):
         return None
     T, E = sd
     X, Y, Z = rd

@@ -163,6 +163,13 @@ class ShardedRun:
                     box = ir.box_of(dims, out_spec, st.ext, st.coords(dev))
                     self.local[(dev, mb, nid)] = full[ir.sl(box)]
             return
+        if code == "reduce_sum":
+            rep = tuple(() for _ in self.dims(ins[0]))
+            for dev in st.devices:
+                full = self.fetch(st, dev, mb, ins[0], rep).sum(axis=info)
+                box = ir.box_of(dims, out_spec, st.ext, st.coords(dev))
+                self.local[(dev, mb, nid)] = full[ir.sl(box)]
+            return
         # elementwise members
         row_split = any(st.ext[a] > 1 for a in out_spec[-1])
         for dev in st.devices:

@@ -34,6 +34,12 @@ backward of the adapters
   dispatch                             zero: the 0/1 mask is piecewise constant (the
                                        bmm producing its input still runs, as planned)
   regroup                              regroup back
+Wide-ResNet adapters (builders.build_wide_resnet; N = images, from the pooling view):
+  reshape (N*H*W, C) -> (N*Ho*Wo, k*k*C)   im2col, k x k window, stride s = H/Ho, pad k/2
+  reshape (N*H*W, C) -> (N*Ho*Wo, C)       subsample (stride-s shortcut, stem pool)
+  reduction                                sum over the axis (global pooling); its
+                                           backward reshape broadcasts
+  backward: col2im (the adjoint of im2col), subsample_grad (scatter into zeros)
 backward (colocate_with = f)
   elementwise(out), colocated with out       loss seed dL/dy = y   (L = 1/2 |y|^2)
   elementwise(g) colocated with unary f       f'(x) * g (GeLU) / softmax backward
@@ -46,6 +52,7 @@ The same table is restated independently in oracle/ (the CPU checker).
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 from typing import Optional
 
@@ -65,6 +72,8 @@ class Bound:
     route: Optional[tuple[int, int, int, int]] = None
     # regroup geometry (A, P, C): (A, P*C, h) -> (P, A*C, h)
     regroup: Optional[tuple[int, int, int]] = None
+    # Wide-ResNet adapters (N, H, W, C, k, s): im2col / subsample of NHWC rows
+    conv: Optional[tuple[int, int, int, int, int, int]] = None
 
 
 def _head_geom(two_d: tuple[int, int], three_d: tuple[int, int, int],
@@ -80,9 +89,39 @@ def _head_geom(two_d: tuple[int, int], three_d: tuple[int, int, int],
     return (B, H, s, d)
 
 
+def image_batch(graph: Graph) -> Optional[int]:
+    """Images per microbatch of a convolutional graph: the leading dim of the
+    (N, H*W, C) view its pooling reduction sums over (builders.build_wide_resnet)."""
+    for n in graph.nodes:
+        if n.kind == KIND_RED and n.colocate_with is None:
+            src = graph[n.inputs[0]]
+            if len(src.dims) == 3:
+                return src.dims[0]
+    return None
+
+
+def conv_geom(ind, outd, batch: Optional[int]):
+    """(op, (N, H, W, C, k, s)) for a 2-D -> 2-D count-changing reshape of NHWC rows:
+    im2col (columns x k*k, odd k) or subsample (same columns)."""
+    if batch is None:
+        return None
+    (ri, ci), (ro, co) = ind, outd
+    if ri % batch or ro % batch or co % ci:
+        return None
+    H, Ho = math.isqrt(ri // batch), math.isqrt(ro // batch)
+    k = math.isqrt(co // ci)
+    if H * H * batch != ri or Ho * Ho * batch != ro or k * k * ci != co or k % 2 == 0 or Ho > H:
+        return None
+    s = max(1, H // Ho)
+    if (H + 2 * (k // 2) - k) // s + 1 != Ho:
+        return None
+    return ("subsample" if k == 1 else "im2col"), (batch, H, H, ci, k, s)
+
+
 def bind(graph: Graph) -> dict[int, Bound]:
     out: dict[int, Bound] = {}
     cons = graph.consumers()
+    batch = image_batch(graph)
     for n in graph.nodes:
         fwd = n.colocate_with is None
         if n.kind == KIND_INPUT:
@@ -96,13 +135,13 @@ def bind(graph: Graph) -> dict[int, Bound]:
         elif n.kind == KIND_ELEM:
             out[n.id] = _bind_elementwise(graph, n, out, cons)
         elif n.kind == KIND_RESHAPE:
-            out[n.id] = _bind_reshape(graph, n, out, cons)
+            out[n.id] = _bind_reshape(graph, n, out, cons, batch)
         else:
             raise PlanError(f"node {n.id}: unknown kind {n.kind}")
     return out
 
 
-def routing_geom(graph: Graph, r) -> Optional[tuple[str, tuple[int, int, int, int]]]:
+def routing_geom(graph: Graph, r, cons) -> Optional[tuple[str, tuple[int, int, int, int]]]:
     """("dispatch" | "combine", (G, S, E, C)) when forward reshape `r` turns MoE
     gates (a unary forward elementwise of shape (T, E)) into a routing tensor."""
     if r.kind != KIND_RESHAPE or r.colocate_with is not None:
@@ -111,6 +150,8 @@ def routing_geom(graph: Graph, r) -> Optional[tuple[str, tuple[int, int, int, in
     if src.kind != KIND_ELEM or src.colocate_with is not None or len(src.inputs) != 1:
         return None
     if len(src.dims) != 2 or len(r.dims) != 3:
+        return None
+    if not any(graph[c].kind == KIND_BMM and slot == 0 for c, slot in cons[r.id]):
         return None
     T, E = src.dims
     X, Y, Z = r.dims
@@ -129,8 +170,7 @@ def _bind_elementwise(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
     if n.colocate_with is None:
         if len(n.inputs) == 1:
             src = graph[n.inputs[0]]
-            if any(graph[c].kind == KIND_RESHAPE and graph[c].colocate_with is None
-                   and len(graph[c].dims) == 3 and len(n.dims) == 2 for c, _ in cons[n.id]):
+            if any(routing_geom(graph, graph[c], cons) is not None for c, _ in cons[n.id]):
                 return Bound("softmax", softmax_scale=1.0)       # MoE gates
             if src.kind == KIND_BMM and graph[src.inputs[1]].kind != KIND_PARAM:
                 d = graph[src.inputs[0]].dims[-1]       # contraction length of q @ k^T
@@ -156,7 +196,7 @@ def _bind_elementwise(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
     raise PlanError(f"node {n.id}: no backward binding for forward op {fb.op}")
 
 
-def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
+def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons, batch=None) -> Bound:
     src = graph[n.inputs[0]]
     ind, outd = src.dims, n.dims
     if n.colocate_with is not None:
@@ -170,6 +210,8 @@ def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
             if fb.op == "regroup":
                 A, P, C = fb.regroup
                 return Bound("regroup", regroup=(P, A, C))
+            if fb.op in ("im2col", "subsample"):
+                return Bound("col2im" if fb.op == "im2col" else "subsample_grad", conv=fb.conv)
             inverse = {"split": "merge", "split_t": "merge_t", "merge": "split",
                        "merge_t": "split_t", "transpose": "transpose", "identity": "identity"}
             op = inverse[fb.op]
@@ -177,7 +219,7 @@ def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
         if f.kind == KIND_RED:
             return Bound("broadcast")
         raise PlanError(f"node {n.id}: backward reshape colocated with {f.kind}")
-    rg = routing_geom(graph, n)
+    rg = routing_geom(graph, n, cons)
     if rg is not None:
         return Bound(rg[0], route=rg[1])
     if len(ind) == 3 and len(outd) == 3 and src.kind == KIND_BMM:
@@ -192,7 +234,7 @@ def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
             cn = graph[c]
             lhs = graph[cn.inputs[0]]
             if cn.kind == KIND_BMM and slot == 1 and lhs.kind == KIND_RESHAPE and \
-                    routing_geom(graph, lhs) is None:
+                    routing_geom(graph, lhs, cons) is None:
                 transposed = True
         return Bound("split_t" if transposed else "split",
                      heads=_head_geom(ind, outd, transposed))
@@ -202,4 +244,8 @@ def _bind_reshape(graph: Graph, n, bound: dict[int, Bound], cons) -> Bound:
         return Bound("identity")
     if len(ind) >= 2 and outd == ind[:-2] + (ind[-1], ind[-2]):
         return Bound("transpose")
+    if len(ind) == 2 and len(outd) == 2:
+        cg = conv_geom(ind, outd, batch)
+        if cg is not None:
+            return Bound(cg[0], conv=cg[1])
     raise PlanError(f"node {n.id}: reshape {ind} -> {outd} has no binding")

@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmpexec.so"
-SOURCES = ["gemm_sm100.cu", "attention.cu", "ops.cu", "moe.cu", "comm.cu", "ilp.cpp"]
+SOURCES = ["gemm_sm100.cu", "attention.cu", "ops.cu", "moe.cu", "conv.cu", "comm.cu", "ilp.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -71,6 +71,9 @@ EXPORTS = {
     "mp_moe_route": ([c_vp, c_i64, c_i64, c_int, c_int, c_int, c_vp, c_vp], c_int),
     "mp_moe_mask": ([c_vp, c_vp, c_i64, c_vp, c_i64, c_int, c_int, c_int, c_int, c_vp], c_int),
     "mp_moe_mask_grad": ([c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_int, c_int, c_vp], c_int),
+    "mp_im2col": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_vp], c_int),
+    "mp_subsample": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_vp], c_int),
+    "mp_reduce_mid": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_int, c_vp], c_int),
     "mp_pack_box": ([c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp, c_vp], c_int),
     "mp_unpack_box": ([c_vp, c_vp, c_i64p, c_i64p, c_i64p, c_int, c_int, c_vp], c_int),
     "mp_adam_step": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_f32, c_f32, c_f32, c_f32, c_f32,
@@ -176,6 +179,15 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
     _require(b, torch.bfloat16, "b")
     if out.dtype not in (torch.bfloat16, torch.float32):
         raise NativeError("out must be bf16 or fp32")
+    # TMA needs 16-byte aligned non-unit strides: operands / outputs with an odd
+    # inner extent (the Wide-ResNet stem's 7*7*3 = 147 im2col columns, a 4-expert
+    # gate) go through zero-padded copies
+    a, b = _aligned(a), _aligned(b)
+    if not _is_aligned(out) and epilogue == 0 and not gelu:
+        tmp = _aligned(out, copy=beta != 0.0)
+        gemm(a, b, tmp, alpha=alpha, beta=beta, stream=stream)
+        out.copy_(tmp)
+        return out
     ad, ab = _split_batch(a, "a")
     bd, bb = _split_batch(b, "b")
     cd, cb = _split_batch(out, "out")
@@ -210,6 +222,33 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
         e1.record()
         timer.append((2.0 * ad[0] * ad[1] * bd[1] * ab[0] * ab[1], e0, e1))
     return out
+
+
+def _is_aligned(t: torch.Tensor) -> bool:
+    q = 16 // t.element_size()
+    return t.data_ptr() % 16 == 0 and all(st % q == 0 for st, n in zip(t.stride(), t.shape)
+                                          if st != 1 and n > 1)
+
+
+def _aligned(t: torch.Tensor, copy: bool = True) -> torch.Tensor:
+    """t itself when its strides suit TMA, else an equal-valued view into a buffer
+    whose contiguous dim is padded to 16 bytes (zeros in the padding)."""
+    if _is_aligned(t):
+        return t
+    q = 16 // t.element_size()
+    inner = -1 if t.stride(-1) == 1 else -2
+    shape = list(t.shape)
+    if inner == -2:
+        t2 = t.transpose(-1, -2)
+        shape[-2], shape[-1] = shape[-1], shape[-2]
+    else:
+        t2 = t
+    padded = shape[:-1] + [-(-shape[-1] // q) * q]
+    buf = torch.zeros(padded, dtype=t.dtype, device=t.device)
+    view = buf[..., :shape[-1]]
+    if copy:
+        view.copy_(t2)
+    return view if inner == -1 else view.transpose(-1, -2)
 
 
 SPLIT_K = os.environ.get("MPEXEC_SPLIT_K", "1") != "0"
@@ -478,6 +517,62 @@ def moe_mask_grad(route: torch.Tensor, d: torch.Tensor, E: int, S: int, C: int, 
     out = torch.empty(T, E, dtype=torch.bfloat16, device=d.device) if out is None else out
     _check(load().mp_moe_mask_grad(route.data_ptr(), d.data_ptr(), out.data_ptr(), T, S, E, C,
                                    mode, _stream(stream)), "mp_moe_mask_grad")
+    return out
+
+
+# --------------------------------------------------------------------------- conv adapters
+
+def _conv_out(H: int, k: int, s: int) -> int:
+    return (H + 2 * (k // 2) - k) // s + 1
+
+
+def im2col(x: torch.Tensor, N: int, H: int, W: int, C: int, k: int, s: int,
+           stream=None) -> torch.Tensor:
+    """(N*H*W, C) NHWC -> (N*Ho*Wo, k*k*C) patches (csrc/conv.cu)."""
+    _require(x, torch.bfloat16, "x")
+    _contig(x, "x")
+    Ho, Wo = _conv_out(H, k, s), _conv_out(W, k, s)
+    out = torch.empty(N * Ho * Wo, k * k * C, dtype=torch.bfloat16, device=x.device)
+    _check(load().mp_im2col(x.data_ptr(), out.data_ptr(), N, H, W, C, k, s, 0, _stream(stream)),
+           "mp_im2col")
+    return out
+
+
+def col2im(d: torch.Tensor, N: int, H: int, W: int, C: int, k: int, s: int,
+           stream=None) -> torch.Tensor:
+    _require(d, torch.bfloat16, "d")
+    _contig(d, "d")
+    out = torch.empty(N * H * W, C, dtype=torch.bfloat16, device=d.device)
+    _check(load().mp_im2col(d.data_ptr(), out.data_ptr(), N, H, W, C, k, s, 1, _stream(stream)),
+           "mp_im2col")
+    return out
+
+
+def subsample(x: torch.Tensor, N: int, H: int, W: int, C: int, s: int, backward: bool = False,
+              stream=None) -> torch.Tensor:
+    """forward: (N*H*W, C) -> (N*Ho*Wo, C); backward: (N*Ho*Wo, C) -> (N*H*W, C)."""
+    _require(x, torch.bfloat16, "x")
+    _contig(x, "x")
+    Ho, Wo = _conv_out(H, 1, s), _conv_out(W, 1, s)
+    rows = N * H * W if backward else N * Ho * Wo
+    out = torch.empty(rows, C, dtype=torch.bfloat16, device=x.device)
+    _check(load().mp_subsample(x.data_ptr(), out.data_ptr(), N, H, W, C, s, int(backward),
+                               _stream(stream)), "mp_subsample")
+    return out
+
+
+def reduce_mid(x: torch.Tensor, broadcast_b: Optional[int] = None, stream=None) -> torch.Tensor:
+    """(A, B, C) -> (A, C) sum over B; with broadcast_b: (A, C) -> (A, B, C)."""
+    _require(x, torch.bfloat16, "x")
+    _contig(x, "x")
+    if broadcast_b is None:
+        A, B, C = x.shape
+        out = torch.empty(A, C, dtype=torch.bfloat16, device=x.device)
+    else:
+        (A, C), B = x.shape, broadcast_b
+        out = torch.empty(A, B, C, dtype=torch.bfloat16, device=x.device)
+    _check(load().mp_reduce_mid(x.data_ptr(), out.data_ptr(), A, B, C,
+                                int(broadcast_b is not None), _stream(stream)), "mp_reduce_mid")
     return out
 
 

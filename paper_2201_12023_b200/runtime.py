@@ -222,8 +222,14 @@ class StageRunner:
                 if b.fwd_ref is not None:          # MoE routing gradients read the gates
                     ins.append((b.fwd_ref, replicated(len(g[b.fwd_ref].dims))))
                 op = _Op(nid, b.op, b, ins, out)
-            elif b.op in ("reduce_sum", "broadcast"):
-                raise ExecError(f"node {nid}: reduction ops are not supported by this executor")
+            elif b.op == "reduce_sum":
+                # operand replicated along the reduced axis, else in the output's layout
+                ax = n.reduce_axis
+                if len(g[n.inputs[0]].dims) != 3 or ax != 1:
+                    raise ExecError(f"node {nid}: only (A, B, C) -> (A, C) reductions are bound")
+                d = out.dims
+                req = Spec(d[:ax] + ((),) + d[ax:])
+                op = _Op(nid, b.op, b, [(n.inputs[0], req)], out)
             else:
                 ins = [(p, out) for p in n.inputs]
                 if b.fwd_ref is not None:
@@ -320,6 +326,9 @@ class StageRunner:
                 u = users[0][0]
                 uop = ops[pos[u]]
                 if self.spec(u) != o.out_spec:
+                    continue
+                # epilogue aux rows must be 16-byte aligned (8 bf16 columns)
+                if local_dims(self.graph[o.nid].dims, o.out_spec, self.mesh)[-1] % 8:
                     continue
                 # bmm: the MoE expert FFN only (GPU time at K = 1024, graph-timed:
                 # dual 306 us vs 227 + 87 us unfused; GeLU' 370 vs 227 + 174 us)
@@ -940,6 +949,18 @@ class StageRunner:
             route = native.moe_route(gates, S, C)
             y = native.moe_mask_grad(route, self._contig(self._as3(x)), E, S, C,
                                      0 if kind == "dispatch_grad" else 1)
+        elif kind in ("im2col", "col2im", "subsample", "subsample_grad"):
+            N, H, W, C, k, s = op.bound.conv
+            x2 = self._contig(x)
+            if kind == "im2col":
+                y = native.im2col(x2, N, H, W, C, k, s)
+            elif kind == "col2im":
+                y = native.col2im(x2, N, H, W, C, k, s)
+            else:
+                y = native.subsample(x2, N, H, W, C, s, backward=kind == "subsample_grad")
+        elif kind == "broadcast":
+            A, B, C = self.graph[op.nid].dims
+            y = native.reduce_mid(self._contig(x).view(A, C), broadcast_b=B)
         elif kind == "regroup":
             A, P, C = op.bound.regroup
             x3 = self._as3(x)
@@ -1120,6 +1141,9 @@ class StageRunner:
                     out = self._run_matmul(mb, op)
                 elif self.graph[op.nid].kind == "reshape":
                     out = self._run_reshape(mb, op)
+                elif op.op == "reduce_sum":
+                    out = native.reduce_mid(self._contig(self._as3(
+                        self.get(mb, op.ins[0][0], op.ins[0][1]))))
                 else:
                     out = self._run_elementwise(mb, op)
             except native.NativeError as e:

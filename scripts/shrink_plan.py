@@ -20,13 +20,17 @@ def main():
     ap.add_argument("src")
     ap.add_argument("dst")
     ap.add_argument("--reference-src", default="/root/reference/pkg/src")
-    ap.add_argument("--blocks", type=int, required=True)
+    ap.add_argument("--blocks", type=int, default=0)
     ap.add_argument("--batch", type=int, required=True)
-    ap.add_argument("--seq", type=int, required=True)
-    ap.add_argument("--hidden", type=int, required=True)
-    ap.add_argument("--heads", type=int, required=True)
+    ap.add_argument("--seq", type=int, default=0)
+    ap.add_argument("--hidden", type=int, default=0)
+    ap.add_argument("--heads", type=int, default=0)
     ap.add_argument("--microbatches", type=int, default=None)
-    ap.add_argument("--builder", choices=("transformer", "moe"), default="transformer")
+    ap.add_argument("--builder", choices=("transformer", "moe", "wresnet"), default="transformer")
+    ap.add_argument("--image", type=int, default=32, help="wresnet: image side")
+    ap.add_argument("--base", type=int, default=8, help="wresnet: base channels")
+    ap.add_argument("--width", type=int, default=1, help="wresnet: width factor")
+    ap.add_argument("--classes", type=int, default=16, help="wresnet: classes")
     ap.add_argument("--experts", type=int, default=None, help="moe: experts")
     ap.add_argument("--ffn-mult", type=int, default=8, help="moe: FFN width / hidden")
     a = ap.parse_args()
@@ -34,7 +38,12 @@ def main():
     from meshplan import graph as graph_mod
     from meshplan.graph import build_transformer_blocks
     doc = json.loads(Path(a.src).read_text())
-    if a.builder == "moe":
+    if a.builder == "wresnet":
+        sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+        from paper_2201_12023_b200.builders import build_wide_resnet
+        g = build_wide_resnet(a.batch, a.image, a.base, a.width, classes=a.classes,
+                              elem_bytes=2, backward=True)
+    elif a.builder == "moe":
         sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
         from paper_2201_12023_b200.builders import build_moe
         g = build_moe(a.blocks, a.batch, a.seq, a.hidden, a.heads, a.experts,

@@ -6,6 +6,10 @@ Tolerances (bf16 storage, fp32 accumulation on the GPU; float64 oracle):
   forward output          relative Frobenius error <= 3e-2
   parameter gradients     relative Frobenius error <= 5e-2 (each parameter), and
                           <= 1e-2 over all parameters together
+  never stricter than      2x the error of the oracle with every node value
+                          rounded to bf16 (bf16_storage_errors): deep graphs
+                          without normalisation (Wide-ResNet, 50 layers) lose
+                          ~2.3% to storage rounding alone
   MoE routing             expert choices equal to the oracle's on every token
                           whose top-3 logit gaps are >= ROUTE_TIE; numerics are
                           compared with the executor's routing replayed
@@ -81,6 +85,28 @@ def routing_margin(doc, params, inputs) -> float:
     return m
 
 
+def bf16_storage_errors(doc, p16, x16, routes, L, G, O) -> dict:
+    """Errors of the float64 oracle with every node's value rounded to bf16 (what
+    bf16 activation storage alone costs on this graph), against the plain oracle."""
+    from oracle import dense
+    orig = dense.eval_node
+
+    def rounded(*a, **k):
+        r = orig(*a, **k)
+        return bf16_round(r).astype(np.float64) if isinstance(r, np.ndarray) else r
+    dense.eval_node = rounded
+    try:
+        L2, G2, O2 = dense.run(doc, p16, x16, doc["num_microbatches"], routes=routes)
+    finally:
+        dense.eval_node = orig
+    out = {"loss": abs(L2 - L) / abs(L), "grad": max((rel(G2[k], G[k]) for k in G), default=0.0),
+           "output": max((rel(O2[m], O[m]) for m in O), default=0.0)}
+    num = sum(float(np.sum((G2[k] - G[k]) ** 2)) for k in G)
+    den = sum(float(np.sum(G[k] ** 2)) for k in G)
+    out["grad_global"] = float(np.sqrt(num / max(den, 1e-300))) if G else 0.0
+    return out
+
+
 def rel(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
@@ -121,6 +147,8 @@ def compare(doc, result, params, inputs):
     L, G, O = dense.run(doc, p16, x16, doc["num_microbatches"], routes=routes)
     errs = {"loss": abs(result.loss - L) / abs(L), "oracle_loss": L, "gpu_loss": result.loss}
     errs.update(route_errs)
+    emu = bf16_storage_errors(doc, p16, x16, routes, L, G, O)
+    errs["bf16_storage"] = emu
     per = {k: rel(result.grads[k], G[k]) for k in G}
     errs["grad"] = max(per.values()) if per else 0.0
     errs["grad_worst"] = sorted(per.items(), key=lambda kv: -kv[1])[:4]
@@ -131,8 +159,14 @@ def compare(doc, result, params, inputs):
     outs = [rel(result.outputs[(mb, y)], O[mb]) for (mb, y) in result.outputs] if result.outputs else [0.0]
     errs["output"] = max(outs)
     tol_grad = TOL["grad"] if _blocks(doc["graph"]["nodes"]) <= 2 else TOL["grad_deep"]
-    errs["ok"] = errs["loss"] <= TOL["loss"] and errs["grad"] <= tol_grad and \
-        errs.get("grad_global", 0.0) <= TOL["grad_global"] and errs["output"] <= TOL["output"] \
+    # never stricter than twice the error of merely storing every node in bf16
+    tol_grad = max(tol_grad, 2 * emu["grad"])
+    tol_glob = max(TOL["grad_global"], 2 * emu["grad_global"])
+    tol_out = max(TOL["output"], 2 * emu["output"])
+    tol_loss = max(TOL["loss"], 2 * emu["loss"])
+    errs["tol"] = {"loss": tol_loss, "grad": tol_grad, "grad_global": tol_glob, "output": tol_out}
+    errs["ok"] = errs["loss"] <= tol_loss and errs["grad"] <= tol_grad and \
+        errs.get("grad_global", 0.0) <= tol_glob and errs["output"] <= tol_out \
         and errs.get("route_mismatch", 0) == 0
     return errs
 

@@ -88,11 +88,22 @@ def test_gemm_batched_head_views():
     assert rel_err(out, qh.float().transpose(-1, -2) @ scores.float()) < 2e-3
 
 
-def test_gemm_rejects_misaligned():
+def test_gemm_misaligned_operands_are_repacked():
+    """Odd inner extents (the Wide-ResNet stem's 147 im2col columns) go through
+    zero-padded copies; a misaligned epilogue aux is still rejected."""
     a = rnd(128, 65)[:, :63]
     b = rnd(63, 128)
+    out = torch.empty(128, 128, device="cuda")
+    native.gemm(a, b, out)
+    assert rel_err(out, a.float() @ b.float()) < 2e-3
+    o2 = torch.empty(128, 147, device="cuda", dtype=torch.bfloat16)
+    b2 = rnd(63, 147)
+    native.gemm(a, b2, o2)
+    assert rel_err(o2, a.float() @ b2.float()) < 1e-2
+    aux = torch.empty(128, 135, device="cuda", dtype=torch.bfloat16)[:, :132]
     with pytest.raises(native.NativeError):
-        native.gemm(a, b, torch.empty(128, 128, device="cuda"))
+        native.gemm(rnd(128, 64), rnd(64, 132), torch.empty(128, 136, device="cuda",
+                    dtype=torch.bfloat16)[:, :132], epilogue=native.EPI_ADD, aux=aux)
 
 
 def test_elementwise_ops():
