@@ -143,3 +143,36 @@ def patch_reference(meshplan_pkg, index: Mapping[str, str], measured: Mapping[st
 
     inter.evaluate_stage = evaluate_stage
     return orig
+
+
+def patch_cross_stage(meshplan_pkg):
+    """SURVEY §8 f4 (the paper's stated limitation): the
+    reference DP prices a stage by compute + intra-stage communication only
+    (`intra.py:511-516`), so T* omits the cross-mesh transfers its own
+    simulator charges (`sim.py:80-84`).  This wraps `evaluate_stage` so each
+    view's t_comm also carries the receive time of the stage's external
+    activations, one `transfer_time` (alpha + bytes / inter_bw, `costs.py:88-92`)
+    per tensor.  Weights are excluded (parameter nodes of the original graph).
+    Opt-in: it changes plans.  Returns the original function."""
+    from dataclasses import replace
+    inter = meshplan_pkg.inter
+    orig = inter.evaluate_stage
+
+    def evaluate_stage(graph_, op_ids, shape, cluster, cost_model, *a, **kw):
+        ev = orig(graph_, op_ids, shape, cluster, cost_model, *a, **kw)
+        params = {i for i, n in enumerate(graph_.nodes) if n.kind.value == "parameter"}
+        views = []
+        for vr in ev.views:
+            specs = vr.plan.node_specs()
+            extra = Fraction(0)
+            for lid in ev.sub.boundary_inputs:
+                if ev.sub.orig_of[lid] in params or lid not in specs:
+                    continue
+                nbytes = ev.sub.graph.node(lid).out_shape.byte_size // \
+                    specs[lid].shard_factor(vr.view)
+                extra += cost_model.transfer_time(nbytes)
+            views.append(replace(vr, report=replace(vr.report, t_comm=vr.report.t_comm + extra)))
+        return type(ev)(ev.sub, tuple(views))
+
+    inter.evaluate_stage = evaluate_stage
+    return orig

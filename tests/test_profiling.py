@@ -97,3 +97,22 @@ def test_patch_reference_swaps_in_measured_times():
     with pytest.raises(KeyError):
         profiling.patch_reference(pkg, {}, {})
         inter.evaluate_stage(None, [1], Shape(1, 1), None, None)
+
+
+@pytest.mark.reference
+def test_cross_stage_cost_in_dp(meshplan_ref, tmp_path):
+    """with the cross-stage receive time inside the DP, config 1
+    plans one (1,4) stage whose T* equals the reference simulator's makespan
+    with modeled transfers (the plain planner's T* is 71% low)."""
+    import subprocess
+    import sys
+    res = subprocess.run([sys.executable, str(ROOT / "scripts/plan_cross_stage.py"),
+                          "--builder", "mlp:layers=2,batch=64,hidden=1024,backward=1",
+                          "--cluster", str(ROOT / "plans/clusters/b200_1x4.json"), "--b", "4",
+                          "--out", str(tmp_path)], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    s = json.loads((tmp_path / "summary.json").read_text())
+    assert len(s["plain"]["stages"]) == 2 and s["plain"]["t_star_error_vs_sim"] > 1.0
+    assert len(s["cross_stage"]["stages"]) == 1
+    assert abs(s["cross_stage"]["t_star_error_vs_sim"]) < 1e-9
+    assert s["cross_stage"]["sim_makespan_s"] < 0.6 * s["plain"]["sim_makespan_s"]
