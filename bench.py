@@ -243,6 +243,7 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     from paper_2201_12023_b200 import native
     from paper_2201_12023_b200.runtime import Executor
+    from paper_2201_12023_b200.schedule import modeled_makespan
 
     plan_path = Path(args.plan)
     doc = json.loads(plan_path.read_text())
@@ -334,6 +335,11 @@ def main():
                      "achieved_basis": "GEMM FLOPs / union of GEMM launch intervals (CUDA events)",
                      "gemm_share_of_step": g_union / t_local if t_local else None,
                      "peak_source": f"{src} bf16_tflops_sustained"},
+        "modeled": {"t_star_s": float(ex.program.t_star),
+                    "sim_makespan_s": float(modeled_makespan(ex.program, ex.plan)),
+                    "basis": "reference cost model (costs.py) / simulator timing rules "
+                             "(sim.py:91-188) restated in schedule.modeled_makespan; "
+                             "compare with ms_per_step"},
         "gpu_launches": launches // args.steps,
         "loss": loss,
         "clocks": clk,

@@ -36,7 +36,7 @@ from .layout import (all_local, allgather_axes, canonical, matmul_algo, relayout
                      reshape_required)
 from .plan import (KIND_PARAM, ExecPlan, Mesh, PlanError, Spec, box_numel, device_box, load_plan,
                    local_dims, replicated)
-from .schedule import GPIPE, Instr, Program, build_program
+from .schedule import GPIPE, Instr, Program, build_program, modeled_makespan
 from .xmesh import recvs_of, sends_of
 
 
@@ -67,6 +67,10 @@ class ExecResult:
     outputs: Optional[dict] = None                  # (microbatch, node) -> global forward output
     gpu_launches: int = 0
     fused: dict = field(default_factory=dict)       # this rank's stage: fused clusters / epilogues
+    # the reference simulator's modeled step for this program (schedule.modeled_makespan,
+    # sim.py:91-188 timing rules) and the planner's T*, beside the measured makespan
+    modeled_makespan: Optional[float] = None
+    t_star: Optional[float] = None
     # MoE routing used (collect=True): (microbatch, gates node) -> int32 (T, 4)
     # {e1, pos1|-1, e2, pos2|-1}, the decisions the parity check replays
     routes: Optional[dict] = None
@@ -1471,6 +1475,8 @@ class Executor:
         peak = {self.rank: int(torch.cuda.max_memory_allocated())}
         r = self.runner
         return ExecResult(makespan=makespan, utilization=util, peak_bytes=peak, events=events,
+                          modeled_makespan=float(modeled_makespan(self.program, self.plan)),
+                          t_star=float(self.program.t_star),
                           loss=self.loss(), step_times=list(self.step_times), grads=grads,
                           outputs=outputs, gpu_launches=launches,
                           fused={"attention": len(r.attn_clusters),

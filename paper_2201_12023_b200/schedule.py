@@ -162,3 +162,75 @@ def build_program(plan: ExecPlan, schedule: str = GPIPE,
         ins.append(Instr("sync", i))
         progs.append(StageProgram(i, tuple(st.mesh.device_ids), st.mem_stage, ins))
     return Program(progs, B, schedule, bwd, plan.t_star, bds)
+
+
+def _frac_of(v) -> Fraction:
+    return Fraction(v[0], v[1]) if isinstance(v, (list, tuple)) else Fraction(v)
+
+
+def modeled_makespan(program: Program, plan: ExecPlan, zero_transfer: bool = False) -> Fraction:
+    """The reference simulator's makespan for this program (sim.py:91-188 timing
+    rules, exact rationals): per stage in instruction order; compute lasts its
+    modeled duration; a send lasts its slowest pair's `transfer_time` (alpha +
+    bytes / inter_bw, costs.py:88-92); a recv ends at max(now, its send's end);
+    an all_gather costs alpha + (g-1)/g * bytes / min axis bandwidth
+    (costs.py:63-73); sync is a barrier across the stages.  Memory accounting
+    is not restated (the executor measures real memory).  This is the modeled
+    comparator printed beside measured B200 times."""
+    cl = plan.cluster
+    alpha, inter_bw = _frac_of(cl["alpha"]), _frac_of(cl["inter_bw"])
+    stages = program.stages
+    n = len(stages)
+    pc, now = [0] * n, [Fraction(0)] * n
+    send_end: dict[str, Fraction] = {}
+
+    def dur(ins: Instr) -> Fraction:
+        if ins.op == "compute":
+            return ins.duration or Fraction(0)
+        if zero_transfer or ins.op in ("alloc", "free", "sync", "recv"):
+            return Fraction(0)
+        if ins.op == "send":
+            return max((alpha + Fraction(b) / inter_bw for *_, b in ins.pairs), default=Fraction(0))
+        if ins.op == "all_gather":
+            st = plan.stages[ins.stage]
+            g = st.mesh.group_extent(ins.axes)
+            if g <= 1:
+                return Fraction(0)
+            bw = min(st.axis_bw[a] for a in ins.axes)
+            return alpha + Fraction((g - 1) * ins.nbytes, g) / bw
+        return Fraction(0)
+
+    total = sum(len(sp.instructions) for sp in stages)
+    done = 0
+    while done < total:
+        progressed = False
+        at_sync = [pc[i] < len(stages[i].instructions) and
+                   stages[i].instructions[pc[i]].op == "sync" for i in range(n)]
+        fin = [pc[i] >= len(stages[i].instructions) for i in range(n)]
+        if all(a or f for a, f in zip(at_sync, fin)) and not all(fin):
+            barrier = max(now[i] for i in range(n) if at_sync[i])
+            for i in range(n):
+                if at_sync[i]:
+                    now[i] = barrier
+                    pc[i] += 1
+                    done += 1
+            continue
+        for i in range(n):
+            while pc[i] < len(stages[i].instructions):
+                ins = stages[i].instructions[pc[i]]
+                if ins.op == "sync":
+                    break
+                if ins.op == "recv":
+                    if ins.tag not in send_end:
+                        break
+                    now[i] = max(now[i], send_end[ins.tag])
+                else:
+                    now[i] += dur(ins)
+                    if ins.op == "send":
+                        send_end[ins.tag] = now[i]
+                pc[i] += 1
+                done += 1
+                progressed = True
+        if not progressed:
+            raise PlanError("deadlock in the instruction lists")
+    return max(now) if now else Fraction(0)

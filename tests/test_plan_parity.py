@@ -235,3 +235,22 @@ def test_live_reference_random_xmesh(meshplan_ref):
 def format_spec_ref(spec):
     from meshplan.sharding import format_spec as f
     return f(spec)
+
+
+def test_modeled_makespan_equals_reference_simulator():
+    """schedule.modeled_makespan restates the reference simulator's timing rules
+    (sim.py:91-188): exact rational equality with the reference's own makespan
+    (golden, tests/golden/make_sim_golden.py) on every committed plan x schedule,
+    modeled and zero transfers."""
+    from fractions import Fraction
+    from paper_2201_12023_b200.plan import load_plan
+    from paper_2201_12023_b200.schedule import build_program, modeled_makespan
+    gold = json.loads((ROOT / "tests/golden/sim_makespans.json").read_text())
+    assert len(gold) >= 30
+    for name, per in gold.items():
+        plan = load_plan(ROOT / "plans" / name / "plan.json")
+        for sch in ("gpipe", "1f1b"):
+            prog = build_program(plan, sch)
+            for zero in (False, True):
+                want = Fraction(*per[f"{sch}{'_zero' if zero else ''}"])
+                assert modeled_makespan(prog, plan, zero_transfer=zero) == want, (name, sch, zero)
