@@ -155,6 +155,16 @@ def run_reference(args):
     return 0
 
 
+def _traffic():
+    """dram read + write bytes of one GEMM launch from the committed ncu --set full
+    capture (profiles/r1_gemm_traffic.json), or None."""
+    p = ROOT / "profiles/r1_gemm_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return {"bytes_per_launch": d["traffic_bytes"], "source": d["source"]}
+
+
 def _plan_flop(doc) -> int:
     per_mb = sum(n["flop"] for n in doc["graph"]["nodes"]
                  if n["kind"] in ("matmul", "batched_matmul"))
@@ -329,7 +339,7 @@ def main():
         "frac_of_peak": {"measured_sustained": step_flop / t / 1e12 / (sus * args.gpus),
                          "datasheet_2250": step_flop / t / 1e12 / (2250.0 * args.gpus)},
         "roofline": {"bound": "tensor", "achieved": ach, "peak": sus, "unit": UNIT,
-                     "frac": ach / sus, "traffic": None,
+                     "frac": ach / sus, "traffic": _traffic(),
                      "kernel": "mp::gemm_bf16_2sm_kernel<256> (tcgen05 cta_group::2)",
                      "launches": g_n, "avg_launch_us": g_time / max(g_n, 1) * 1e6,
                      "achieved_basis": "GEMM FLOPs / union of GEMM launch intervals (CUDA events)",
