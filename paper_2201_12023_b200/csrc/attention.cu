@@ -88,6 +88,39 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Packed fp32 pairs (Blackwell FFMA2 / FADD2) and the 3-input FMNMX3: the
+// forward softmax is issue-bound in its 4 softmax warps (not MUFU-bound: moving
+// a share of the exponentials to an FMA-pipe polynomial made it slower), so
+// the per-element instruction count is what sets its speed.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 // Store 8 bf16 (one 16-byte unit) of row r, unit u of a 128B-swizzled chunk
 // (explicit st.shared: a generic store would go through the LSU's generic path).
 __device__ __forceinline__ void st_sw128(uint8_t* chunk, int r, int u, uint4 v) {
@@ -243,7 +276,8 @@ __global__ void __launch_bounds__(192, 2)
         tmem_ld32(tS + lane_off + c * 32, t32);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(t32[e]));
+        for (int e = 0; e < 32; e += 2)
+          mx = fmax3(mx, __uint_as_float(t32[e]), __uint_as_float(t32[e + 1]));
       }
       mx *= p.scale_log2;
       // lazy rescale: only when the max grows by more than 2^8
@@ -281,7 +315,8 @@ __global__ void __launch_bounds__(192, 2)
         }
       }
       l *= alpha;
-      float sum = 0.f;
+      const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2), nm2 = f2pack(-m_used, -m_used);
+      uint64_t sum2 = f2pack(0.f, 0.f);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t t32[32];
@@ -297,16 +332,22 @@ __global__ void __launch_bounds__(192, 2)
         for (int t = 0; t < 4; ++t) {
           float pv[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            pv[e] = ex2(__uint_as_float(t32[t * 8 + e]) * p.scale_log2 - m_used);
-            sum += pv[e];
+          for (int e = 0; e < 8; e += 2) {
+            float x0, x1;
+            f2unpack(ffma2(f2pack(__uint_as_float(t32[t * 8 + e]),
+                                  __uint_as_float(t32[t * 8 + e + 1])), sc2, nm2), x0, x1);
+            pv[e] = ex2(x0);
+            pv[e + 1] = ex2(x1);
+            sum2 = fadd2(sum2, f2pack(pv[e], pv[e + 1]));
           }
           st_sw128(chunk, r, (c & 1) * 4 + t,
                    make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]),
                               pack_bf2(pv[4], pv[5]), pack_bf2(pv[6], pv[7])));
         }
       }
-      l += sum;
+      float s0, s1;
+      f2unpack(sum2, s0, s1);
+      l += s0 + s1;
       fence_async_smem();
       tc_fence_before();
       __syncwarp();
@@ -471,8 +512,10 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          sts32(smem_u32(sLse + st * 128 + k * 32 + lane), nl[k] * 1.4426950408889634f);
-          sts32(smem_u32(sD + st * 128 + k * 32 + lane), nd[k]);
+          // staged negated and pre-scaled for the packed P / dS math:
+          // -LSE * log2(e) and -D * scale
+          sts32(smem_u32(sLse + st * 128 + k * 32 + lane), nl[k] * -1.4426950408889634f);
+          sts32(smem_u32(sD + st * 128 + k * 32 + lane), nd[k] * -p.scale);
         }
         mbar_arrive(&q_full[st]);   // release: publishes the lse / D stores
         if (i == 0) {                // K / V of this tile once the previous tile is done with them
@@ -558,6 +601,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     const int r = q * 32 + lane;                        // key row (S^T / dP^T lane)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float sl2 = p.scale * 1.4426950408889634f;
+    const uint64_t sl2_2 = f2pack(sl2, sl2), sc_2 = f2pack(p.scale, p.scale);
     int g = 0, t = 0;
     for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++t) {
       for (int i = 0; i < n_q; ++i, ++g) {
@@ -599,15 +643,20 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
             lse2[4 * k] = a.x; lse2[4 * k + 1] = a.y; lse2[4 * k + 2] = a.z; lse2[4 * k + 3] = a.w;
             dvv[4 * k] = bq.x; dvv[4 * k + 1] = bq.y; dvv[4 * k + 2] = bq.z; dvv[4 * k + 3] = bq.w;
           }
+          // P = 2^(S * scale * log2e - LSE * log2e), dS = P * (dP * scale - D * scale)
+          // in packed fp32 pairs (scale = 2^-3 at d = 64: bit-identical to the
+          // unpacked P * (dP - D) * scale)
           float pv[16], ds[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-  #ifdef MP_FA_EXP_TEST
-          pv[e] = fmaf(__uint_as_float(s16[e]), sl2, -lse2[e]);
-#else
-          pv[e] = ex2(fmaf(__uint_as_float(s16[e]), sl2, -lse2[e]));
-#endif
-            ds[e] = pv[e] * (__uint_as_float(d16[e]) - dvv[e]) * p.scale;
+          for (int e = 0; e < 16; e += 2) {
+            float x0, x1;
+            f2unpack(ffma2(f2pack(__uint_as_float(s16[e]), __uint_as_float(s16[e + 1])), sl2_2,
+                           f2pack(lse2[e], lse2[e + 1])), x0, x1);
+            pv[e] = ex2(x0);
+            pv[e + 1] = ex2(x1);
+            f2unpack(fmul2(f2pack(pv[e], pv[e + 1]),
+                           ffma2(f2pack(__uint_as_float(d16[e]), __uint_as_float(d16[e + 1])), sc_2,
+                                 f2pack(dvv[e], dvv[e + 1]))), ds[e], ds[e + 1]);
           }
           const int ch = c >> 2, u0 = (c & 3) * 2;
           st_sw128(pt + ch * FA_TILE, r, u0,
