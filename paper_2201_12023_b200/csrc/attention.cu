@@ -268,17 +268,21 @@ __global__ void __launch_bounds__(192, 2)
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(s_full, j & 1);
       tc_fence_after();
-      // pass 1: row max (TMEM re-read in pass 2 is cheaper than holding 128 registers)
+      // The whole S row (128 fp32) moves to registers at once, so S is released
+      // before the max: the next S = Q K^T runs under this tile's exp / P pass.
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + lane_off + c * 32, sv[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t t32[32];
-        tmem_ld32(tS + lane_off + c * 32, t32);
-        tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int e = 0; e < 32; e += 2)
-          mx = fmax3(mx, __uint_as_float(t32[e]), __uint_as_float(t32[e + 1]));
-      }
+          mx = fmax3(mx, __uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1]));
       mx *= p.scale_log2;
       // lazy rescale: only when the max grows by more than 2^8
       const bool need = (mx > m_used + 8.f);
@@ -317,16 +321,9 @@ __global__ void __launch_bounds__(192, 2)
       l *= alpha;
       const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2), nm2 = f2pack(-m_used, -m_used);
       uint64_t sum2 = f2pack(0.f, 0.f);
-#pragma unroll 1
+#pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t t32[32];
-        tmem_ld32(tS + lane_off + c * 32, t32);
-        tmem_ld_wait();
-        if (c == 3) {   // S fully read: let the next S = Q K^T overwrite it
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(s_free);
-        }
+        const uint32_t(&t32)[32] = sv[c];
         uint8_t* chunk = sP + (c >> 1) * FA_TILE;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
