@@ -117,7 +117,8 @@ int mp_softmax_rowdot(const void* y, const void* dy, float* rowdot, int64_t rows
  * structural backward graph.py:341-361), for stages whose softmax dim is local.
  * Q/K/V/O/dO/dK/dV: (B*s, ld) bf16 row-major, head hh in columns [hh*d, hh*d+d);
  * d must be 64, s a multiple of 128.  lse, dvec: fp32 [B*H, s].  dq_acc: fp32
- * (B*s, ld), zeroed by the caller, accumulated atomically (cast afterwards).
+ * (B*s, ld), zeroed by the call itself (its D pre-pass), then accumulated by TMA bulk
+ * reductions (cast afterwards).
  * Non-causal softmax(scale * q k^T). */
 int mp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                 int64_t B, int64_t H, int64_t s, int64_t d, int64_t ld, float scale,

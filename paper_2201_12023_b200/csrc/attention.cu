@@ -769,9 +769,11 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
   }
 }
 
-// D[bh, t] = sum_d dO * O   (warp per row of 64), and dQacc zeroing is done by the caller
+// D[bh, t] = sum_d dO * O   (warp per row of 64); the same pass zeroes the row's
+// dQ accumulator (the backward adds into it with TMA bulk reductions)
 __global__ void fa_bwd_pre_kernel(const uint16_t* __restrict__ O, const uint16_t* __restrict__ dO,
-                                  float* __restrict__ dvec, int B, int H, int s, int ld) {
+                                  float* __restrict__ dvec, float* __restrict__ dq_acc, int B,
+                                  int H, int s, int ld) {
   const int lane = threadIdx.x & 31;
   const int64_t rows = (int64_t)B * H * s;
   const int64_t wpb = blockDim.x >> 5;
@@ -781,6 +783,7 @@ __global__ void fa_bwd_pre_kernel(const uint16_t* __restrict__ O, const uint16_t
     const int64_t off = (b * s + t) * ld + hh * FA_D + lane * 2;
     uint32_t o = *reinterpret_cast<const uint32_t*>(O + off);
     uint32_t g = *reinterpret_cast<const uint32_t*>(dO + off);
+    *reinterpret_cast<float2*>(dq_acc + off) = make_float2(0.f, 0.f);
     float acc = bf2f(o & 0xffff) * bf2f(g & 0xffff) + bf2f(o >> 16) * bf2f(g >> 16);
 #pragma unroll
     for (int k = 16; k; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
@@ -946,8 +949,8 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
                "bad pointers");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   fa_bwd_pre_kernel<<<row_warps_grid(B * H * s), 256, 0, st>>>(
-      reinterpret_cast<const uint16_t*>(o), reinterpret_cast<const uint16_t*>(dout), dvec, (int)B,
-      (int)H, (int)s, (int)ld);
+      reinterpret_cast<const uint16_t*>(o), reinterpret_cast<const uint16_t*>(dout), dvec, dq_acc,
+      (int)B, (int)H, (int)s, (int)ld);
   MP_CHECK_LAUNCH();
   CUtensorMap mq, mk, mv, mdo, mdq;
   int rc;

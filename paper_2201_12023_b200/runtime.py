@@ -584,7 +584,7 @@ class StageRunner:
         Bl, Hl = T // s, hdim // d
         k0, k1 = cl["kv"]
         dvec = torch.empty(Bl * Hl, s, dtype=torch.float32, device=self.dev)
-        dq_acc = torch.zeros(T, hdim, dtype=torch.float32, device=self.dev)
+        dq_acc = torch.empty(T, hdim, dtype=torch.float32, device=self.dev)   # zeroed by the pre pass
         dk = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
         dv = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
         native.attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, Bl, Hl, s, d, cl["scale"],
