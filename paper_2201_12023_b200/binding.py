@@ -91,7 +91,10 @@ def _head_geom(two_d: tuple[int, int], three_d: tuple[int, int, int],
 
 def image_batch(graph: Graph) -> Optional[int]:
     """Images per microbatch of a convolutional graph: the leading dim of the
-    (N, H*W, C) view its pooling reduction sums over (builders.build_wide_resnet)."""
+    (N, H*W, C) view its pooling reduction sums over (builders.build_wide_resnet),
+    or the plan's `image_batch` hint for a stage sub-graph without the head."""
+    if getattr(graph, "image_batch", None):
+        return graph.image_batch
     for n in graph.nodes:
         if n.kind == KIND_RED and n.colocate_with is None:
             src = graph[n.inputs[0]]

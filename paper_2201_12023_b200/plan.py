@@ -218,6 +218,9 @@ class Node:
 class Graph:
     nodes: tuple[Node, ...]
     outputs: tuple[int, ...]
+    # images per microbatch of a convolutional graph when the graph itself cannot
+    # tell (a stage sub-graph without the pooling head; plan config "image_batch")
+    image_batch: Optional[int] = None
 
     def __len__(self) -> int:
         return len(self.nodes)
@@ -325,6 +328,8 @@ def load_plan(src: Union[str, Path, dict]) -> ExecPlan:
     if doc.get("kind") != PLAN_KIND or doc.get("version") != 1:
         raise PlanError("not a meshplan plan document")
     graph = graph_from_doc(doc["graph"])
+    if doc.get("config", {}).get("image_batch"):
+        graph = Graph(graph.nodes, graph.outputs, int(doc["config"]["image_batch"]))
     stages = []
     for sd in doc["stages"]:
         mesh = Mesh(int(sd["logical_view"][0]), int(sd["logical_view"][1]),

@@ -80,9 +80,15 @@ def stage_doc(graph_doc: dict, op_ids: Iterable[int], view: tuple[int, int],
     cl.setdefault("alpha", [1, 100000])
     cl.setdefault("device_flops", [1400000000000000, 1])
     cl.setdefault("device_memory", 180000000000)
+    config = {"profile_stage": True}
+    for n in nodes:      # convolutional graphs: keep the image count the binding needs
+        if n["kind"].startswith("reduction") and "colocate_with" not in n:
+            src = nodes[n["inputs"][0][0]]["shape"]["dims"]
+            if len(src) == 3:
+                config["image_batch"] = int(src[0])
     return {
         "version": 1, "kind": PLAN_KIND,
-        "config": {"profile_stage": True},
+        "config": config,
         "cluster": cl,
         "graph": {"version": graph_doc.get("version", 1), "nodes": out_nodes, "outputs": outputs},
         "num_microbatches": int(num_microbatches),
@@ -118,10 +124,12 @@ def candidate_key(op_ids: Iterable[int], shape: tuple[int, int], view: tuple[int
 
 
 def patch_reference(meshplan_pkg, index: Mapping[str, str], measured: Mapping[str, float],
-                    strict: bool = True):
+                    strict: bool = True, missing: str = "model"):
     """Wrap `meshplan.inter.evaluate_stage` so every view report carries the
     measured seconds per microbatch of its candidate (index: candidate key ->
-    doc key; measured: doc key -> seconds).  Returns the original function."""
+    doc key; measured: doc key -> seconds).  Unmeasured candidates raise (strict),
+    keep the analytic cost (missing="model") or are priced out (missing="exclude").
+    Returns the original function."""
     from dataclasses import replace
     inter = meshplan_pkg.inter
     orig = inter.evaluate_stage
@@ -135,7 +143,11 @@ def patch_reference(meshplan_pkg, index: Mapping[str, str], measured: Mapping[st
             if dk is None or dk not in measured:
                 if strict:
                     raise KeyError(f"no measurement for candidate {ck}")
-                views.append(vr)
+                if missing == "exclude":    # unmeasured candidates are never chosen
+                    views.append(replace(vr, report=replace(
+                        vr.report, t_compute=Fraction(10 ** 9), t_comm=Fraction(0))))
+                else:
+                    views.append(vr)
                 continue
             t = Fraction(measured[dk]).limit_denominator(10**12)
             views.append(replace(vr, report=replace(vr.report, t_compute=t, t_comm=Fraction(0))))

@@ -51,7 +51,8 @@ def cmd_emit(a):
     from meshplan.sharding import format_spec
     from paper_2201_12023_b200 import ilp, profiling
     ilp.patch_reference(mp)
-    graph = cli._parse_builder(a.builder)
+    graph = (cli._parse_builder(a.builder) if a.builder
+             else graph_mod.parse(Path(a.graph).read_bytes()))
     cdoc = json.loads(Path(a.cluster).read_text())
     cluster = cluster_from_json(cdoc)
     gdoc = json.loads(graph_mod.serialize(graph))
@@ -65,7 +66,7 @@ def cmd_emit(a):
         for hi in range(lo + 1, a.layers + 1):
             ops = clustering.range_ops(lo, hi)
             for shape in admissible_shapes(cluster):
-                if shape.num_devices > cluster.num_devices:
+                if shape.num_devices > cluster.num_devices or shape.num_devices > a.max_devices:
                     continue
                 ev = evaluate_stage(graph, ops, shape, cluster, cm)
                 for vr in ev.views:
@@ -160,7 +161,8 @@ def cmd_plan(a):
     d = Path(a.dir)
     idx = json.loads((d / "index.json").read_text())
     measured = json.loads((d / "measured.json").read_text())
-    profiling.patch_reference(mp, idx["candidates"], measured, strict=not a.lenient)
+    profiling.patch_reference(mp, idx["candidates"], measured, strict=not (a.lenient or a.measured_only),
+                              missing="exclude" if a.measured_only else "model")
     rest = a.rest[1:] if a.rest[:1] == ["--"] else a.rest
     return cli.main(["plan", *rest, "--out", a.out])
 
@@ -169,10 +171,13 @@ def main():
     ap = argparse.ArgumentParser()
     sub = ap.add_subparsers(dest="cmd", required=True)
     e = sub.add_parser("emit")
-    e.add_argument("--builder", required=True)
+    e.add_argument("--builder", default=None)
+    e.add_argument("--graph", default=None, help="reference graph JSON (e.g. from builders.py)")
     e.add_argument("--cluster", required=True)
     e.add_argument("--layers", type=int, required=True)
     e.add_argument("--microbatches", type=int, default=2)
+    e.add_argument("--max-devices", type=int, default=1 << 30,
+                   help="only candidates on submeshes of at most this many devices")
     e.add_argument("--out", required=True)
     e.add_argument("--reference-src", default="/root/reference/pkg/src")
     r = sub.add_parser("run")
@@ -184,6 +189,8 @@ def main():
     p.add_argument("--out", required=True)
     p.add_argument("--lenient", action="store_true",
                    help="keep the analytic cost for candidates without a measurement")
+    p.add_argument("--measured-only", action="store_true",
+                   help="candidates without a measurement are inadmissible (infinite cost)")
     p.add_argument("--reference-src", default="/root/reference/pkg/src")
     p.add_argument("rest", nargs=argparse.REMAINDER)
     a = ap.parse_args()
