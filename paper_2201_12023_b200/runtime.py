@@ -267,6 +267,8 @@ class StageRunner:
         self.tok_dw: dict[int, tuple[int, ...]] = {}
         if os.environ.get("MPEXEC_TOKEN_SPLIT_DW", "1") != "0":
             self._token_split_dw()
+        self.local_conv = (self._local_conv()
+                           if os.environ.get("MPEXEC_LOCAL_CONV", "1") != "0" else {})
 
     def have_spec(self, nid: int) -> Spec:
         """Layout the node's value is actually stored in."""
@@ -306,6 +308,29 @@ class StageRunner:
             if all(c == o.nid for c, _ in self.cons[a]) and a not in self.out_ids:
                 drop.add(a)
         self.bwd_ops = [o for o in self.bwd_ops if o.nid not in drop]
+
+    def _local_conv(self) -> dict[int, tuple[int, ...]]:
+        """Wide-ResNet adapters on row-split activations.  The planner makes every
+        im2col / subsample reshape (and its backward) a layout barrier: replicated
+        in, replicated out (intra.py:149-160), i.e. an all-gather of the activation
+        on every device.  When the operand's rows are split over mesh axes A in
+        whole images (S^A on dim 0, N divisible by the A-group), each device's image
+        block maps to a contiguous row block of the output, so the adapter runs on
+        the local images and its value is kept row-split (`actual`); consumers
+        that want it that way (the S^A R matmuls of data-parallel stages) read it
+        with no communication, others reshard on demand."""
+        out = {}
+        for op in self.fwd_ops + self.bwd_ops:
+            if op.op not in ("im2col", "col2im", "subsample", "subsample_grad") or \
+                    op.nid in self.out_ids:
+                continue
+            sp = self.spec(op.ins[0][0])
+            if len(sp.dims) != 2 or not sp.dims[0] or sp.dims[1]:
+                continue
+            A = tuple(sp.dims[0])
+            if op.bound.conv[0] % self.mesh.group_extent(A) == 0:
+                out[op.nid] = A
+        return out
 
     def _fuse_epilogues(self) -> int:
         """Fold a matmul's single trivial consumer into its GEMM epilogue:
@@ -934,6 +959,20 @@ class StageRunner:
             native.gemm(a, b, out, beta=beta, epilogue=epilogue, aux=aux)
 
     def _run_reshape(self, mb: int, op: _Op) -> torch.Tensor:
+        A = self.local_conv.get(op.nid)
+        if A is not None:                     # row-split conv adapter (see _local_conv)
+            rs = Spec((A, ()))
+            x = self._contig(self.get(mb, op.ins[0][0], rs))
+            N, H, W, C, k, s = op.bound.conv
+            Nl = N // self.mesh.group_extent(A)
+            if op.op == "im2col":
+                y = native.im2col(x, Nl, H, W, C, k, s)
+            elif op.op == "col2im":
+                y = native.col2im(x, Nl, H, W, C, k, s)
+            else:
+                y = native.subsample(x, Nl, H, W, C, s, backward=op.op == "subsample_grad")
+            self.actual[op.nid] = rs
+            return y
         x = self.get(mb, op.ins[0][0], op.ins[0][1])
         kind = op.op
         if kind == "identity":
@@ -1483,6 +1522,7 @@ class Executor:
                                  "attention_key_split": sum(1 for c in r.attn_clusters
                                                             if c["key_axes"]),
                                  "epilogues": r.fused_epilogues,
+                                 "local_conv": len(r.local_conv),
                                  "token_split_dw": len(r.tok_dw)})
 
 
