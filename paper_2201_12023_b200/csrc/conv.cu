@@ -6,6 +6,8 @@
 // im2col column order is (ky, kx, c); padding p = k/2 reads zeros.
 // All of these move bytes (HBM-bound); the backward forms are gathers, so every
 // output element is written once in a fixed summation order (deterministic).
+#include <type_traits>
+#include <cstring>
 #include "common.cuh"
 #include "../../include/mp_exec.h"
 
@@ -24,75 +26,110 @@ struct ConvGeom {
   int k, s, p;
 };
 
-// out[(n, oy, ox), (ky, kx, c)] = in[(n, oy*s+ky-p, ox*s+kx-p), c]; V = elements per access
+// out[(n, oy, ox), (ky, kx, c)] = in[(n, oy*s+ky-p, ox*s+kx-p), c]; V = elements per
+// access (8: one 16-byte vector when C % 8 == 0).  32-bit index math (element
+// counts < 2^31 are checked on the host): the 64-bit div/mod chain made these
+// byte-moving kernels instruction-bound.
 template <int V>
 __global__ void im2col_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
                               ConvGeom g) {
-  const int64_t cv = g.C / V, kk = (int64_t)g.k * g.k;
-  const int64_t total = g.N * g.Ho * g.Wo * kk * cv;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
-    int64_t c = i % cv, r = i / cv;
-    int64_t tap = r % kk;
+  const int cv = (int)(g.C / V), kk = g.k * g.k;
+  const int Ho = (int)g.Ho, Wo = (int)g.Wo, H = (int)g.H, W = (int)g.W;
+  const int total = (int)(g.N * g.Ho * g.Wo) * kk * cv;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int c = i % cv;
+    int r = i / cv;
+    const int tap = r % kk;
     r /= kk;
-    int64_t ox = r % g.Wo, t = r / g.Wo, oy = t % g.Ho, n = t / g.Ho;
-    int64_t y = oy * g.s + tap / g.k - g.p, x = ox * g.s + tap % g.k - g.p;
+    const int ox = r % Wo, t = r / Wo, oy = t % Ho, n = t / Ho;
+    const int ky = tap / g.k, kx = tap - ky * g.k;
+    const int y = oy * g.s + ky - g.p, x = ox * g.s + kx - g.p;
+    const bool in_img = y >= 0 && y < H && x >= 0 && x < W;
     if (V == 8) {
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (y >= 0 && y < g.H && x >= 0 && x < g.W)
-        v = reinterpret_cast<const uint4*>(in)[((n * g.H + y) * g.W + x) * cv + c];
+      if (in_img) v = reinterpret_cast<const uint4*>(in)[((int64_t)(n * H + y) * W + x) * cv + c];
       reinterpret_cast<uint4*>(out)[i] = v;
     } else {
-      uint16_t v = 0;
-      if (y >= 0 && y < g.H && x >= 0 && x < g.W) v = in[((n * g.H + y) * g.W + x) * g.C + c];
-      out[i] = v;
+      out[i] = in_img ? in[((int64_t)(n * H + y) * W + x) * g.C + c] : (uint16_t)0;
     }
   }
 }
 
-// dx[(n, y, x), c] = sum over taps (ky, kx) with (y + p - ky) = oy*s, (x + p - kx) = ox*s
-// in range of dcol[(n, oy, ox), (ky, kx, c)]  (fp32 accumulation, fixed tap order)
+// dx[(n, y, x), c] = sum over taps (ky, kx) with y + p - ky = oy*s, x + p - kx = ox*s
+// in range of dcol[(n, oy, ox), (ky, kx, c)]  (fp32 accumulation, fixed tap order;
+// 8 channels per thread when C % 8 == 0)
+template <int V>
 __global__ void col2im_kernel(const uint16_t* __restrict__ dcol, uint16_t* __restrict__ dx,
                               ConvGeom g) {
-  const int64_t total = g.N * g.H * g.W * g.C, kkc = (int64_t)g.k * g.k * g.C;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
-    int64_t c = i % g.C, r = i / g.C;
-    int64_t x = r % g.W, t = r / g.W, y = t % g.H, n = t / g.H;
-    float acc = 0.f;
+  const int cv = (int)(g.C / V), kkc = g.k * g.k * (int)g.C;
+  const int Ho = (int)g.Ho, Wo = (int)g.Wo, H = (int)g.H, W = (int)g.W;
+  const int total = (int)(g.N * g.H * g.W) * cv;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int c = (i % cv) * V;
+    const int r = i / cv;
+    const int x = r % W, t = r / W, y = t % H, n = t / H;
+    float acc[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] = 0.f;
     for (int ky = 0; ky < g.k; ++ky) {
-      int64_t yy = y + g.p - ky;
+      const int yy = y + g.p - ky;
       if (yy < 0 || yy % g.s) continue;
-      int64_t oy = yy / g.s;
-      if (oy >= g.Ho) continue;
+      const int oy = yy / g.s;
+      if (oy >= Ho) continue;
       for (int kx = 0; kx < g.k; ++kx) {
-        int64_t xx = x + g.p - kx;
+        const int xx = x + g.p - kx;
         if (xx < 0 || xx % g.s) continue;
-        int64_t ox = xx / g.s;
-        if (ox >= g.Wo) continue;
-        acc += bf2f(dcol[((n * g.Ho + oy) * g.Wo + ox) * kkc + (ky * g.k + kx) * g.C + c]);
+        const int ox = xx / g.s;
+        if (ox >= Wo) continue;
+        const int64_t off = ((int64_t)(n * Ho + oy) * Wo + ox) * kkc + (ky * g.k + kx) * (int)g.C + c;
+        if (V == 8) {
+          const uint4 v = *reinterpret_cast<const uint4*>(dcol + off);
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc[2 * e] += bf2f(w[e] & 0xffff);
+            acc[2 * e + 1] += bf2f(w[e] >> 16);
+          }
+        } else {
+          acc[0] += bf2f(dcol[off]);
+        }
       }
     }
-    dx[i] = f2bf(acc);
+    if (V == 8) {
+      reinterpret_cast<uint4*>(dx)[i] = make_uint4(pack_bf2(acc[0], acc[1]), pack_bf2(acc[2], acc[3]),
+                                                   pack_bf2(acc[4], acc[5]), pack_bf2(acc[6], acc[7]));
+    } else {
+      dx[i] = f2bf(acc[0]);
+    }
   }
 }
 
 // out[(n, oy, ox), c] = in[(n, oy*s, ox*s), c]; grad: dx = dy at those pixels, else 0
+// (V channels per thread: 8 = one 16-byte vector when C % 8 == 0)
+template <int V>
 __global__ void subsample_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
                                  ConvGeom g, int backward) {
-  const int64_t total = backward ? g.N * g.H * g.W * g.C : g.N * g.Ho * g.Wo * g.C;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
-    int64_t c = i % g.C, r = i / g.C;
+  using T = typename std::conditional<V == 8, uint4, uint16_t>::type;
+  const T* src = reinterpret_cast<const T*>(in);
+  T* dst = reinterpret_cast<T*>(out);
+  const int cv = (int)(g.C / V);
+  const int Ho = (int)g.Ho, Wo = (int)g.Wo, H = (int)g.H, W = (int)g.W;
+  const int total = (backward ? (int)(g.N * g.H * g.W) : (int)(g.N * g.Ho * g.Wo)) * cv;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int c = i % cv, r = i / cv;
     if (!backward) {
-      int64_t ox = r % g.Wo, t = r / g.Wo, oy = t % g.Ho, n = t / g.Ho;
-      out[i] = in[((n * g.H + oy * g.s) * g.W + ox * g.s) * g.C + c];
+      const int ox = r % Wo, t = r / Wo, oy = t % Ho, n = t / Ho;
+      dst[i] = src[((int64_t)(n * H + oy * g.s) * W + ox * g.s) * cv + c];
     } else {
-      int64_t x = r % g.W, t = r / g.W, y = t % g.H, n = t / g.H;
-      uint16_t v = 0;
-      if (y % g.s == 0 && x % g.s == 0 && y / g.s < g.Ho && x / g.s < g.Wo)
-        v = in[((n * g.Ho + y / g.s) * g.Wo + x / g.s) * g.C + c];
-      out[i] = v;
+      const int x = r % W, t = r / W, y = t % H, n = t / H;
+      T v;
+      memset(&v, 0, sizeof(T));
+      if (y % g.s == 0 && x % g.s == 0 && y / g.s < Ho && x / g.s < Wo)
+        v = src[((int64_t)(n * Ho + y / g.s) * Wo + x / g.s) * cv + c];
+      dst[i] = v;
     }
   }
 }
@@ -138,17 +175,22 @@ int mp_im2col(const void* x, void* out, int64_t N, int64_t H, int64_t W, int64_t
                "bad args");
   ConvGeom g = geom(N, H, W, C, k, s);
   cudaStream_t st = MP_STREAM(stream);
+  MP_CHECK_ARG(N * H * W * C < (1LL << 31) && N * g.Ho * g.Wo * k * k * C < (1LL << 31),
+               "tensor too large for 32-bit indexing");
+  const bool vec = C % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(out) % 16 == 0;
   if (!backward) {
-    bool vec = C % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
-               reinterpret_cast<uintptr_t>(out) % 16 == 0;
     int64_t n = N * g.Ho * g.Wo * k * k * (vec ? C / 8 : C);
     if (vec)
       im2col_kernel<8><<<grid_of(n, 256), 256, 0, st>>>((const uint16_t*)x, (uint16_t*)out, g);
     else
       im2col_kernel<1><<<grid_of(n, 256), 256, 0, st>>>((const uint16_t*)x, (uint16_t*)out, g);
   } else {
-    col2im_kernel<<<grid_of(N * H * W * C, 256), 256, 0, st>>>((const uint16_t*)x,
-                                                               (uint16_t*)out, g);
+    int64_t n = N * H * W * (vec ? C / 8 : C);
+    if (vec)
+      col2im_kernel<8><<<grid_of(n, 256), 256, 0, st>>>((const uint16_t*)x, (uint16_t*)out, g);
+    else
+      col2im_kernel<1><<<grid_of(n, 256), 256, 0, st>>>((const uint16_t*)x, (uint16_t*)out, g);
   }
   MP_CHECK_LAUNCH();
   return 0;
@@ -159,9 +201,16 @@ int mp_subsample(const void* x, void* out, int64_t N, int64_t H, int64_t W, int6
   clear_error();
   MP_CHECK_ARG(x && out && N > 0 && H > 0 && W > 0 && C > 0 && s >= 1, "bad args");
   ConvGeom g = geom(N, H, W, C, 1, s);
-  int64_t n = backward ? N * H * W * C : N * g.Ho * g.Wo * C;
-  subsample_kernel<<<grid_of(n, 256), 256, 0, MP_STREAM(stream)>>>((const uint16_t*)x,
-                                                                   (uint16_t*)out, g, backward);
+  MP_CHECK_ARG(N * H * W * C < (1LL << 31), "tensor too large for 32-bit indexing");
+  const bool vec = C % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  int64_t n = (backward ? N * H * W : N * g.Ho * g.Wo) * (vec ? C / 8 : C);
+  if (vec)
+    subsample_kernel<8><<<grid_of(n, 256), 256, 0, MP_STREAM(stream)>>>(
+        (const uint16_t*)x, (uint16_t*)out, g, backward);
+  else
+    subsample_kernel<1><<<grid_of(n, 256), 256, 0, MP_STREAM(stream)>>>(
+        (const uint16_t*)x, (uint16_t*)out, g, backward);
   MP_CHECK_LAUNCH();
   return 0;
 }
