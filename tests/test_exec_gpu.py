@@ -19,7 +19,8 @@ SINGLE = ["plans/mlp_n1/plan.json", "plans/tiny_gpt_n1/plan.json",
           "plans/tiny_gpt_deep_n1/plan.json"]
 MULTI = [("plans/mlp_n2/plan.json", 2), ("plans/tiny_gpt_n2/plan.json", 2),
          ("plans/tiny_gpt_n4/plan.json", 4), ("plans/cfg1/plan.json", 4),
-         ("plans/tiny_gpt_n8/plan.json", 8), ("plans/tiny_gpt_tp_n4/plan.json", 4)]
+         ("plans/tiny_gpt_n8/plan.json", 8), ("plans/tiny_gpt_pp_n8/plan.json", 8),
+         ("plans/tiny_gpt_tp_n4/plan.json", 4)]
 
 
 @pytest.mark.parametrize("plan", SINGLE)

@@ -18,7 +18,8 @@ import pytest
 from parity_harness import synth
 
 ROOT = Path(__file__).resolve().parent.parent
-SMALL = ["cfg1", "mlp_n1", "mlp_n2", "tiny_gpt_n1", "tiny_gpt_n2", "tiny_gpt_n4", "tiny_gpt_n8"]
+SMALL = ["cfg1", "mlp_n1", "mlp_n2", "tiny_gpt_n1", "tiny_gpt_n2", "tiny_gpt_n4", "tiny_gpt_n8",
+         "tiny_gpt_pp_n8"]
 
 
 def doc_of(name):
@@ -152,17 +153,20 @@ def _gloo_worker(rank, world, port, plan_name, q):
         dist.destroy_process_group()
 
 
-def test_gloo_two_rank_boundary_exchange():
-    """Host logic of the N>1 path on CPU: ranks 0/1 of the 2-stage plan derive
-    matching send/recv lists and the received boxes carry the right data."""
+@pytest.mark.parametrize("plan,world,port", [("tiny_gpt_n2", 2, 29611), ("tiny_gpt_n8", 8, 29621),
+                                             ("tiny_gpt_pp_n8", 8, 29641),
+                                             ("moe_tiny_n4", 4, 29631)])
+def test_gloo_boundary_exchange(plan, world, port):
+    """Host logic of the N>1 path on CPU: every rank of the plan derives matching
+    send/recv lists and the received boxes carry the right data (world 8: the
+    driver's 8-GPU run, which this pool cannot host)."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29611
-    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, "tiny_gpt_n2", q)) for r in range(2)]
+    ps = [ctx.Process(target=_gloo_worker, args=(r, world, port, plan, q)) for r in range(world)]
     for p in ps:
         p.start()
     for p in ps:
-        p.join(120)
-    res = dict(q.get(timeout=5) for _ in range(2))
-    assert res == {0: True, 1: True}
+        p.join(300)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert res == {r: True for r in range(world)}
