@@ -115,26 +115,28 @@ def all_local(dims, src: Spec, dst: Spec, mesh: Mesh) -> bool:
     return all(is_local_slice(dims, src, dst, mesh, d) for d in mesh.device_ids)
 
 
-def allgather_axes(dims, have: Spec, req: Spec, mesh: Mesh) -> Optional[tuple[int, ...]]:
-    """Mesh axes A such that, on every device, the `req` tile is the dim-0
-    concatenation (in device-id order, i.e. NCCL group rank order) of the
-    `have` tiles of its A-axis group — then one all-gather into the output
-    realises the relayout (e.g. S^1R -> RR); None otherwise."""
+def allgather_axes(dims, have: Spec, req: Spec, mesh: Mesh, dim: int = 0) -> Optional[tuple[int, ...]]:
+    """Mesh axes A such that, on every device, the `req` tile is the concatenation
+    along `dim` (in device-id order, i.e. NCCL group rank order) of the `have`
+    tiles of its A-axis group — then one all-gather realises the relayout (e.g.
+    S^1R -> RR along dim 0 straight into the output; RS^1 -> RR along dim 1
+    through a staging buffer and one permuting copy); None otherwise."""
     found = None
     for d in mesh.device_ids:
         need = device_box(dims, req, mesh, d)
         members = [e for e in sorted(mesh.device_ids)
                    if _contains(need, device_box(dims, have, mesh, e))]
         boxes = [device_box(dims, have, mesh, e) for e in members]
-        if len(members) < 2 or any(b[1:] != need[1:] for b in boxes):
+        if len(members) < 2 or any(b[:dim] + b[dim + 1:] != need[:dim] + need[dim + 1:]
+                                   for b in boxes):
             return None
-        cut = need[0][0]
-        step = (need[0][1] - need[0][0]) // len(members)
+        cut = need[dim][0]
+        step = (need[dim][1] - need[dim][0]) // len(members)
         for b in boxes:
-            if b[0] != (cut, cut + step):
+            if b[dim] != (cut, cut + step):
                 return None
             cut += step
-        if cut != need[0][1] or any(device_box(dims, req, mesh, e) != need for e in members):
+        if cut != need[dim][1] or any(device_box(dims, req, mesh, e) != need for e in members):
             return None
         axes = next((ax for ax in ((0,), (1,), (0, 1)) if mesh.group_extent(ax) > 1
                      and mesh.axis_group(d, ax) == tuple(members)), None)

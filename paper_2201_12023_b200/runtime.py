@@ -85,6 +85,7 @@ class AdamConfig:
     weight_decay: float = 0.0
 
 
+GATHER_ANY_DIM = os.environ.get("MPEXEC_GATHER_ANY_DIM", "1") != "0"
 FUSE_BMM_EPI = os.environ.get("MPEXEC_FUSE_BMM_EPILOGUE", "1") == "1"
 
 
@@ -653,6 +654,18 @@ class StageRunner:
             self.comm.all_gather_into(out.view(-1), src.view(-1),
                                       self.comm.axis_group(self.st.index, self.mesh, info, self.me))
             return out
+        if kind == "allgather_dim":
+            # gather into a (g, *tile) staging buffer, then one copy that moves
+            # the group dim next to `d` (member blocks concatenated along d)
+            axes, d = info
+            src = self._contig(v).view(*local_dims(dims, have, self.mesh))
+            g = self.mesh.group_extent(axes)
+            stage = torch.empty((g,) + tuple(src.shape), dtype=v.dtype, device=self.dev)
+            self.comm.all_gather_into(stage.view(-1), src.view(-1),
+                                      self.comm.axis_group(self.st.index, self.mesh, axes, self.me))
+            perm = stage.movedim(0, d)
+            return native.pack_box(perm, (0,) * perm.dim(), tuple(perm.shape)).view(
+                *local_dims(dims, req, self.mesh))
         return self._relayout(self._as3(v), tuple(dims), have, req)
 
     # ------------------------------------------------------------------ params
@@ -815,7 +828,13 @@ class StageRunner:
             pl = ("local", [(lo - o, hi - lo) for (lo, hi), (o, _) in zip(want, mine)])
         else:
             axes = allgather_axes(dims, have, req, m)
-            pl = ("allgather", axes) if axes is not None else ("p2p", None)
+            pl = ("allgather", axes) if axes is not None else None
+            for d in range(1, len(dims)):
+                if pl is None and GATHER_ANY_DIM:
+                    axes = allgather_axes(dims, have, req, m, dim=d)
+                    pl = ("allgather_dim", (axes, d)) if axes is not None else None
+            if pl is None:
+                pl = ("p2p", None)
         self._plans[key] = pl
         return pl
 

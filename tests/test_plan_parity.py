@@ -152,17 +152,24 @@ def test_allgather_fast_path_is_exact(view):
     m = mesh(view, 0)
     dims = (8, 16)
     glob = np.arange(np.prod(dims)).reshape(dims)
-    hits = 0
+    hits = [0, 0]
     for src, dst in itertools.product(_all_specs(2, m, dims), repeat=2):
-        axes = allgather_axes(dims, src, dst, m)
-        if axes is None:
-            continue
-        hits += 1
-        for d in m.device_ids:
-            grp = m.axis_group(d, axes)
-            cat = np.concatenate([glob[ir.sl(device_box(dims, src, m, e))] for e in grp], 0)
-            assert np.array_equal(cat, glob[ir.sl(device_box(dims, dst, m, d))])
-    assert hits > 0
+        for cdim in (0, 1):         # dim 0: straight into the output; dim 1: staged + permuted
+            axes = allgather_axes(dims, src, dst, m, dim=cdim)
+            if axes is None:
+                continue
+            hits[cdim] += 1
+            for d in m.device_ids:
+                grp = m.axis_group(d, axes)
+                tiles = [glob[ir.sl(device_box(dims, src, m, e))] for e in grp]
+                cat = np.concatenate(tiles, cdim)
+                assert np.array_equal(cat, glob[ir.sl(device_box(dims, dst, m, d))])
+                # the executor's staging: (g, *tile) -> move g next to cdim -> merge
+                stage = np.stack(tiles, 0)
+                perm = np.moveaxis(stage, 0, cdim)
+                merged = perm.reshape(cat.shape)
+                assert np.array_equal(merged, cat)
+    assert hits[0] > 0 and hits[1] > 0
 
 
 def _all_specs(rank, m, dims):
