@@ -40,6 +40,8 @@ struct GemmParams {
   int64_t aux_ld, aux_bs0, aux_bs1;
   int n_wide;         // 2-CTA kernel: tiles [0, n_wide) are 256 x BN; the rest are
                       // half-width splits of the last partial wave (wave-quantisation fix)
+  int c_red;          // 2-CTA kernel, fp32 C += alpha * acc: the epilogue hands each 32 x 16
+                      // block to a TMA bulk reduce-add (L2 does the read-modify-write)
 };
 
 // tile t -> (batch, m block, n block); the faster index is the one with fewer
@@ -352,7 +354,8 @@ struct Gemm2Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 6 : 8;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_STAGE = kEpiWarps * 32 * 16 * 4;   // 32 rows x 16 fp32 per warp
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_STAGE;
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -406,6 +409,28 @@ __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
       : "memory");
 }
 
+// smem -> global fp32 add of a {16 cols, 32 rows, 1, 1} box (TMA reduction)
+__device__ __forceinline__ void tma_reduce_add_4d(const void* tmap, const void* src, int c0, int c1,
+                                                  int c2, int c3) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group"
+      " [%0, {%2, %3, %4, %5}], [%1];" ::"l"(tmap),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_commit_g() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_g() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all_g() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 struct Tile2 {
   int b0, b1, mb, n0;
   bool narrow;
@@ -430,7 +455,8 @@ template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB,
-                         const __grid_constant__ CUtensorMap tmBn, const GemmParams p) {
+                         const __grid_constant__ CUtensorMap tmBn,
+                         const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
   using Cfg = Gemm2Cfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -443,6 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi_stage = smem + STAGES * Cfg::STAGE_BYTES + 256;   // c_red staging (128B aligned)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -575,7 +602,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         const int n = tl.n0 + c * 32;
-        if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r, b0, b1);
+        if (p.c_red) {
+          // fp32 C += alpha * acc without reading C: rows of this warp -> staging ->
+          // TMA reduce-add (out-of-range rows / columns are clipped by the map)
+          float* stg = reinterpret_cast<float*>(epi_stage) + (warp - 2) * 32 * 16;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            if (lane == 0) bulk_wait_read_g();     // the previous box has left the buffer
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<float4*>(stg + lane * 16)[i] =
+                  make_float4(__uint_as_float(r[sub * 16 + 4 * i]) * p.alpha,
+                              __uint_as_float(r[sub * 16 + 4 * i + 1]) * p.alpha,
+                              __uint_as_float(r[sub * 16 + 4 * i + 2]) * p.alpha,
+                              __uint_as_float(r[sub * 16 + 4 * i + 3]) * p.alpha);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_reduce_add_4d(&tmC, stg, n + sub * 16, m - lane, b1, b0);
+              bulk_commit_g();
+            }
+          }
+        } else if (m < p.M && n < p.N) {
+          store_chunk<BN>(p, row_off, m, n, r, b0, b1);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -583,6 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (p.c_red && lane == 0) bulk_wait_all_g();   // staging reads and C adds complete
   }
 
   tc_fence_before();
@@ -643,6 +695,37 @@ static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, 
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed with code " + std::to_string((int)r));
+    return 1;
+  }
+  return 0;
+}
+
+// fp32 C as a reduce-add target: {N, M, nb1, nb0}, box {16, 32, 1, 1}, no swizzle
+static int make_map_f32_red(CUtensorMap* map, void* base, int64_t n, int64_t m, int64_t ldc,
+                            int64_t nb1, int64_t bs1, int64_t nb0, int64_t bs0) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 1;
+  }
+  if (nb1 <= 1) bs1 = ldc * m;
+  if (nb0 <= 1) bs0 = bs1 * (nb1 < 1 ? 1 : nb1);
+  cuuint64_t dims[4] = {(cuuint64_t)n, (cuuint64_t)m, (cuuint64_t)(nb1 < 1 ? 1 : nb1),
+                        (cuuint64_t)(nb0 < 1 ? 1 : nb0)};
+  cuuint64_t strides[3] = {(cuuint64_t)(ldc * 4), (cuuint64_t)(bs1 * 4), (cuuint64_t)(bs0 * 4)};
+  for (int i = 0; i < 3; ++i) {
+    if (strides[i] % 16 != 0 || strides[i] == 0) {
+      set_error("fp32 C stride not a multiple of 16 bytes");
+      return 2;
+    }
+  }
+  cuuint32_t box[4] = {16, 32, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (C) failed with code " + std::to_string((int)r));
     return 1;
   }
   return 0;
@@ -726,7 +809,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams 
 
 template <int BN>
 static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbn,
-                           GemmParams p, cudaStream_t stream) {
+                           const CUtensorMap& mc, GemmParams p, cudaStream_t stream) {
   using Cfg = Gemm2Cfg<BN>;
   static bool configured = false;
   if (!configured) {
@@ -751,7 +834,7 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   if (!no_split && BN == 256 && wide > pairs && r > 0 && 2 * r <= pairs) p.n_wide = wide - r;
   p.num_tiles = p.n_wide + 2 * (wide - p.n_wide);
   if (p.num_tiles < pairs) pairs = p.num_tiles;
-  gemm_bf16_2sm_kernel<BN><<<2 * pairs, kThreads, Cfg::SMEM, stream>>>(ma, mb, mbn, p);
+  gemm_bf16_2sm_kernel<BN><<<2 * pairs, kThreads, Cfg::SMEM, stream>>>(ma, mb, mbn, mc, p);
   return 0;
 }
 
@@ -876,9 +959,18 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
   if (rc) return rc;
 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // fp32 C += alpha * A B (the dW accumulations): TMA reduce-add epilogue
+  static const bool no_red = getenv("MPEXEC_GEMM_NO_REDUCE_EPI") != nullptr;
+  CUtensorMap mc = mb;
+  p.c_red = 0;
+  if (two_sm && c_dtype == 1 && beta == 1.f && epilogue == 0 && !no_red) {
+    rc = make_map_f32_red(&mc, C, N, M, cd[2], nbatch1, cd[5], nbatch0, cd[4]);
+    if (rc) return rc;
+    p.c_red = 1;
+  }
   if (two_sm)
-    rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, mbn, p, s)
-                     : launch_gemm_2sm<128>(ma, mb, mbn, p, s);
+    rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, mbn, mc, p, s)
+                     : launch_gemm_2sm<128>(ma, mb, mbn, mc, p, s);
   else if (BN == 256)
     rc = launch_gemm<256>(ma, mb, p, s);
   else if (BN == 128)
