@@ -302,6 +302,21 @@ def main():
         g_union += cur_e - cur_s
     g_union *= 1e-3
 
+    # ---- GEMM roofline without overlap: one extra step with the dW side stream off,
+    # every GEMM launch timed alone (CUDA events on its own stream); the timed
+    # region above overlaps dW GEMMs with attention, which inflates per-launch spans
+    dw_stream = ex.runner.dw_stream
+    ex.runner.dw_stream = None
+    native.gemm_timer = []
+    torch.cuda.synchronize()
+    ex.runner.run_step(record=False, update=True)
+    torch.cuda.synchronize()
+    serial = native.gemm_timer
+    native.gemm_timer = None
+    ex.runner.dw_stream = dw_stream
+    s_flop = sum(f for f, _, _ in serial)
+    s_time = sum(a.elapsed_time(b) for _, a, b in serial) * 1e-3
+
     # ---- e2e through the public API: H2D inputs from pinned host, D2H loss
     e2e = None
     if not args.no_e2e:
@@ -329,7 +344,8 @@ def main():
             dist.destroy_process_group()
         return 0
     sus, burst, hbm, src = peaks()
-    ach = g_flop / g_union / 1e12 if g_union > 0 else 0.0
+    ach = s_flop / s_time / 1e12 if s_time > 0 else 0.0
+    ach_overlap = g_flop / g_union / 1e12 if g_union > 0 else 0.0
     out = {
         "metric": METRIC, "value": step_flop / t / 1e12, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -341,8 +357,13 @@ def main():
         "roofline": {"bound": "tensor", "achieved": ach, "peak": sus, "unit": UNIT,
                      "frac": ach / sus, "traffic": _traffic(),
                      "kernel": "mp::gemm_bf16_2sm_kernel<256> (tcgen05 cta_group::2)",
-                     "launches": g_n, "avg_launch_us": g_time / max(g_n, 1) * 1e6,
-                     "achieved_basis": "GEMM FLOPs / union of GEMM launch intervals (CUDA events)",
+                     "launches": len(serial), "avg_launch_us": s_time / max(len(serial), 1) * 1e6,
+                     "achieved_basis": "GEMM FLOPs / sum of per-launch durations (CUDA events on "
+                                       "the launching stream), one serialized step (dW side "
+                                       "stream off) right after the timed region",
+                     "achieved_in_step_overlapped": ach_overlap,
+                     "in_step_basis": "timed region: GEMM FLOPs / union of GEMM launch intervals "
+                                      "(dW GEMMs overlap attention on a side stream)",
                      "gemm_share_of_step": g_union / t_local if t_local else None,
                      "peak_source": f"{src} bf16_tflops_sustained"},
         "modeled": {"t_star_s": float(ex.program.t_star),

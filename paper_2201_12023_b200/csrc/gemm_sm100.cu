@@ -42,6 +42,8 @@ struct GemmParams {
                       // half-width splits of the last partial wave (wave-quantisation fix)
   int c_red;          // 2-CTA kernel, fp32 C += alpha * acc: the epilogue hands each 32 x 16
                       // block to a TMA bulk reduce-add (L2 does the read-modify-write)
+  int aux_tma;        // 2-CTA kernel, epilogues 2/3: the aux block of the next 32-column chunk
+                      // is TMA-loaded into the warp's staging buffer ahead of its use
 };
 
 // tile t -> (batch, m block, n block); the faster index is the one with fewer
@@ -72,7 +74,8 @@ struct GemmCfg {
 
 template <int BN>
 __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off, int m, int n,
-                                            const uint32_t (&r)[32], int b0 = 0, int b1 = 0) {
+                                            const uint32_t (&r)[32], int b0 = 0, int b1 = 0,
+                                            const float* apre = nullptr) {
   // r: 32 consecutive fp32 accumulator columns [n, n+32) of row m
   float v[32];
 #pragma unroll
@@ -99,7 +102,10 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off
       }
     } else {
       float a[32];
-      if (n + 32 <= p.N) {
+      if (apre != nullptr) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) a[i] = apre[i];
+      } else if (n + 32 <= p.N) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint4 u = reinterpret_cast<const uint4*>(ax)[i];
@@ -456,7 +462,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmBn,
-                         const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+                         const __grid_constant__ CUtensorMap tmC,
+                         const __grid_constant__ CUtensorMap tmX, const GemmParams p) {
   using Cfg = Gemm2Cfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -469,7 +476,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* epi_stage = smem + STAGES * Cfg::STAGE_BYTES + 256;   // c_red staging (128B aligned)
+  uint8_t* epi_stage = smem + STAGES * Cfg::STAGE_BYTES + 256;   // c_red / aux staging (128B aligned)
+  uint64_t* aux_bar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kEpiWarps]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -487,6 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * kEpiWarps);
     }
+    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -586,6 +595,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    uint32_t aux_phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = pair; t < p.num_tiles; t += npairs) {
@@ -594,15 +604,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int64_t row_off = (int64_t)b0 * p.c_bs0 + (int64_t)b1 * p.c_bs1;
       const int m = tl.mb * 2 * BM + rank * BM + row;
       const int width = tl.narrow ? BN / 2 : BN;
+      const int c_lo = half * (width / 64), c_hi = (half + 1) * (width / 64);
+      uint16_t* ast = reinterpret_cast<uint16_t*>(epi_stage + (warp - 2) * 2048);   // 32 x 32 bf16
+      if (p.aux_tma && lane == 0) {        // first chunk's aux, under the mainloop's tail
+        mbar_arrive_expect_tx(&aux_bar[warp - 2], 2048);
+        tma_load_4d(&tmX, &aux_bar[warp - 2], ast, tl.n0 + c_lo * 32, m - lane, b1, b0);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * (width / 64); c < (half + 1) * (width / 64); ++c) {
+      for (int c = c_lo; c < c_hi; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         const int n = tl.n0 + c * 32;
-        if (p.c_red) {
+        if (p.aux_tma) {
+          mbar_wait(&aux_bar[warp - 2], aux_phase);
+          aux_phase ^= 1;
+          float a[32];
+          const uint4* src = reinterpret_cast<const uint4*>(ast + lane * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint4 u = src[i];
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              a[8 * i + 2 * j] = bf2f(w4[j] & 0xffff);
+              a[8 * i + 2 * j + 1] = bf2f(w4[j] >> 16);
+            }
+          }
+          __syncwarp();                      // buffer read by every lane: refill it
+          if (c + 1 < c_hi && lane == 0) {
+            mbar_arrive_expect_tx(&aux_bar[warp - 2], 2048);
+            tma_load_4d(&tmX, &aux_bar[warp - 2], ast, n + 32, m - lane, b1, b0);
+          }
+          if (m < p.M && n < p.N) store_chunk<BN>(p, row_off, m, n, r, b0, b1, a);
+        } else if (p.c_red) {
           // fp32 C += alpha * acc without reading C: rows of this warp -> staging ->
           // TMA reduce-add (out-of-range rows / columns are clipped by the map)
           float* stg = reinterpret_cast<float*>(epi_stage) + (warp - 2) * 32 * 16;
@@ -700,9 +737,11 @@ static int make_map(CUtensorMap* map, const void* base, int64_t d0, int64_t d1, 
   return 0;
 }
 
-// fp32 C as a reduce-add target: {N, M, nb1, nb0}, box {16, 32, 1, 1}, no swizzle
-static int make_map_f32_red(CUtensorMap* map, void* base, int64_t n, int64_t m, int64_t ldc,
-                            int64_t nb1, int64_t bs1, int64_t nb0, int64_t bs0) {
+// epilogue-side maps (fp32 C reduce-add target, bf16 aux source): {N, M, nb1, nb0},
+// box {box0, 32, 1, 1}, no swizzle
+static int make_map_box(CUtensorMap* map, void* base, CUtensorMapDataType dt, int64_t eb,
+                        int64_t n, int64_t m, int64_t ldc, int64_t nb1, int64_t bs1, int64_t nb0,
+                        int64_t bs0, int box0) {
   auto enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -712,16 +751,16 @@ static int make_map_f32_red(CUtensorMap* map, void* base, int64_t n, int64_t m, 
   if (nb0 <= 1) bs0 = bs1 * (nb1 < 1 ? 1 : nb1);
   cuuint64_t dims[4] = {(cuuint64_t)n, (cuuint64_t)m, (cuuint64_t)(nb1 < 1 ? 1 : nb1),
                         (cuuint64_t)(nb0 < 1 ? 1 : nb0)};
-  cuuint64_t strides[3] = {(cuuint64_t)(ldc * 4), (cuuint64_t)(bs1 * 4), (cuuint64_t)(bs0 * 4)};
+  cuuint64_t strides[3] = {(cuuint64_t)(ldc * eb), (cuuint64_t)(bs1 * eb), (cuuint64_t)(bs0 * eb)};
   for (int i = 0; i < 3; ++i) {
     if (strides[i] % 16 != 0 || strides[i] == 0) {
-      set_error("fp32 C stride not a multiple of 16 bytes");
+      set_error("epilogue operand stride not a multiple of 16 bytes");
       return 2;
     }
   }
-  cuuint32_t box[4] = {16, 32, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)box0, 32, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, estr,
+  CUresult r = enc(map, dt, 4, base, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -809,7 +848,8 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, GemmParams 
 
 template <int BN>
 static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbn,
-                           const CUtensorMap& mc, GemmParams p, cudaStream_t stream) {
+                           const CUtensorMap& mc, const CUtensorMap& mx, GemmParams p,
+                           cudaStream_t stream) {
   using Cfg = Gemm2Cfg<BN>;
   static bool configured = false;
   if (!configured) {
@@ -834,7 +874,7 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   if (!no_split && BN == 256 && wide > pairs && r > 0 && 2 * r <= pairs) p.n_wide = wide - r;
   p.num_tiles = p.n_wide + 2 * (wide - p.n_wide);
   if (p.num_tiles < pairs) pairs = p.num_tiles;
-  gemm_bf16_2sm_kernel<BN><<<2 * pairs, kThreads, Cfg::SMEM, stream>>>(ma, mb, mbn, mc, p);
+  gemm_bf16_2sm_kernel<BN><<<2 * pairs, kThreads, Cfg::SMEM, stream>>>(ma, mb, mbn, mc, mx, p);
   return 0;
 }
 
@@ -964,13 +1004,24 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
   CUtensorMap mc = mb;
   p.c_red = 0;
   if (two_sm && c_dtype == 1 && beta == 1.f && epilogue == 0 && !no_red) {
-    rc = make_map_f32_red(&mc, C, N, M, cd[2], nbatch1, cd[5], nbatch0, cd[4]);
+    rc = make_map_box(&mc, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, N, M, cd[2], nbatch1, cd[5],
+                      nbatch0, cd[4], 16);
     if (rc) return rc;
     p.c_red = 1;
   }
+  // epilogues reading aux (residual add, GeLU'): TMA-staged aux chunks
+  static const bool no_aux_tma = getenv("MPEXEC_GEMM_NO_AUX_TMA") != nullptr;
+  CUtensorMap mx = mb;
+  p.aux_tma = 0;
+  if (two_sm && (epilogue == 2 || epilogue == 3) && !no_aux_tma) {
+    rc = make_map_box(&mx, aux, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, M, aux_desc[0], nbatch1,
+                      aux_desc[2], nbatch0, aux_desc[1], 32);
+    if (rc) return rc;
+    p.aux_tma = 1;
+  }
   if (two_sm)
-    rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, mbn, mc, p, s)
-                     : launch_gemm_2sm<128>(ma, mb, mbn, mc, p, s);
+    rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, mbn, mc, mx, p, s)
+                     : launch_gemm_2sm<128>(ma, mb, mbn, mc, mx, p, s);
   else if (BN == 256)
     rc = launch_gemm<256>(ma, mb, p, s);
   else if (BN == 128)
