@@ -234,3 +234,18 @@ def test_gemm_split_k_accumulate(M, N, K, ta):
     ref = base + a.float() @ b.float()
     assert rel_err(out, ref) < 2e-3
     assert rel_err(out, ref1) < 1e-5
+
+
+@pytest.mark.parametrize("batch,M,N,K,alpha", [(1, 1000, 520, 136, 1.0), (3, 384, 272, 64, 0.5),
+                                               (1, 2048, 2048, 8192, 1.0), (2, 520, 1032, 256, 2.0)])
+def test_gemm_f32_accumulate_reduce_epilogue(batch, M, N, K, alpha):
+    """fp32 C += alpha * A B on the 2-CTA kernel leaves through TMA bulk reduce-adds
+    (partial tiles clipped by the tensor map, batched C); same as torch fp32."""
+    a = rnd(batch, K, M).transpose(-1, -2)      # the dW layout: X^T
+    b = rnd(batch, K, N)
+    c0 = torch.randn(batch, M, N, device="cuda")
+    out = c0.clone()
+    native.gemm(a if batch > 1 else a[0], b if batch > 1 else b[0],
+                out if batch > 1 else out[0], alpha=alpha, beta=1.0)
+    ref = c0 + alpha * (a.float() @ b.float())
+    assert rel_err(out, ref) < 2e-3
