@@ -52,7 +52,10 @@ CASES = [  # batch, M, N, K, ta, tb, f32 (beta=1 accumulate), epilogue
     (1, 8192, 1024, 1024, 0, 0, 0, 0), (1, 8192, 1024, 1024, 0, 1, 0, 0),
     (1, 8192, 8192, 1024, 0, 0, 0, 4), (1, 8192, 8192, 1024, 0, 1, 0, 3),
     (8, 2048, 1024, 1024, 0, 1, 0, 0), (8, 1024, 1024, 2048, 0, 0, 0, 0),
-    (1, 8192, 2048, 2048, 0, 0, 0, 0), (1, 2048, 2048, 8192, 1, 0, 1, 0),
+    (1, 8192, 2048, 2048, 0, 0, 0, 0), (1, 8192, 2048, 2048, 0, 0, 1, 0),
+    (1, 8192, 8192, 2048, 0, 0, 0, 0), (1, 8192, 8192, 2048, 0, 0, 1, 0),
+    (1, 8192, 8192, 2048, 0, 0, 0, 4), (1, 8192, 8192, 2048, 0, 1, 0, 3),
+    (1, 2048, 2048, 8192, 1, 0, 1, 0),
 ]
 for batch, M, N, K, ta, tb, f32, epi in CASES:
     a, b, out = mk(batch, M, N, K, ta, tb, f32)
