@@ -774,20 +774,31 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
 __global__ void fa_bwd_pre_kernel(const uint16_t* __restrict__ O, const uint16_t* __restrict__ dO,
                                   float* __restrict__ dvec, float* __restrict__ dq_acc, int B,
                                   int H, int s, int ld) {
-  const int lane = threadIdx.x & 31;
-  const int64_t rows = (int64_t)B * H * s;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t w = blockIdx.x * wpb + (threadIdx.x >> 5); w < rows; w += (int64_t)gridDim.x * wpb) {
-    const int64_t bh = w / s, t = w - (w / s) * s;
-    const int64_t b = bh / H, hh = bh - (bh / H) * H;
-    const int64_t off = (b * s + t) * ld + hh * FA_D + lane * 2;
-    uint32_t o = *reinterpret_cast<const uint32_t*>(O + off);
-    uint32_t g = *reinterpret_cast<const uint32_t*>(dO + off);
-    *reinterpret_cast<float2*>(dq_acc + off) = make_float2(0.f, 0.f);
-    float acc = bf2f(o & 0xffff) * bf2f(g & 0xffff) + bf2f(o >> 16) * bf2f(g >> 16);
+  // D[r] = sum_d dO[r,d] * O[r,d] and dQ accumulator zeroing: 8 lanes per row, one
+  // 16-byte vector of O and dO per lane (a warp covers 4 rows), 32-bit row math
+  const int lane = threadIdx.x & 31, g = lane >> 3, sub = lane & 7;
+  const int rows = B * H * s;
+  const int warps = (int)((gridDim.x * blockDim.x) >> 5);
+  for (int w4 = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); w4 * 4 < rows; w4 += warps) {
+    const int r = w4 * 4 + g;
+    float acc = 0.f;
+    if (r < rows) {
+      const int bh = r / s, t = r - bh * s;
+      const int b = bh / H, hh = bh - b * H;
+      const int64_t off = ((int64_t)b * s + t) * ld + hh * FA_D + sub * 8;
+      const uint4 o = __ldg(reinterpret_cast<const uint4*>(O + off));
+      const uint4 gg = __ldg(reinterpret_cast<const uint4*>(dO + off));
+      float4* dq = reinterpret_cast<float4*>(dq_acc + off);
+      dq[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      dq[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t ow[4] = {o.x, o.y, o.z, o.w}, gw[4] = {gg.x, gg.y, gg.z, gg.w};
 #pragma unroll
-    for (int k = 16; k; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
-    if (lane == 0) dvec[w] = acc;
+      for (int j = 0; j < 4; ++j)
+        acc += bf2f(ow[j] & 0xffff) * bf2f(gw[j] & 0xffff) + bf2f(ow[j] >> 16) * bf2f(gw[j] >> 16);
+    }
+#pragma unroll
+    for (int k = 4; k; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
+    if (sub == 0 && r < rows) dvec[r] = acc;
   }
 }
 
@@ -948,7 +959,8 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
                    dvec && dq_acc,
                "bad pointers");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  fa_bwd_pre_kernel<<<row_warps_grid(B * H * s), 256, 0, st>>>(
+  MP_CHECK_ARG(B * H * s < (1LL << 31) && ld % 8 == 0, "attention rows exceed int32 / ld not 8-aligned");
+  fa_bwd_pre_kernel<<<row_warps_grid((B * H * s + 3) / 4), 256, 0, st>>>(
       reinterpret_cast<const uint16_t*>(o), reinterpret_cast<const uint16_t*>(dout), dvec, dq_acc,
       (int)B, (int)H, (int)s, (int)ld);
   MP_CHECK_LAUNCH();

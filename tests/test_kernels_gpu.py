@@ -249,3 +249,27 @@ def test_gemm_f32_accumulate_reduce_epilogue(batch, M, N, K, alpha):
                 out if batch > 1 else out[0], alpha=alpha, beta=1.0)
     ref = c0 + alpha * (a.float() @ b.float())
     assert rel_err(out, ref) < 2e-3
+
+
+@pytest.mark.parametrize("nb,M,N,K", [(3, 512, 768, 256), (2, 600, 520, 136)])
+def test_gemm_fused_epilogues_batched(nb, M, N, K):
+    """Batched 2-CTA tiles: bf16 C (and the dual epilogue's GeLU output) leave
+    through TMA tensor stores from swizzled staging; the batched aux-reading
+    epilogues keep direct stores.  Ragged M / N exercise the stores' clipping."""
+    a, b = rnd(nb, M, K), rnd(nb, K, N, scale=0.1)
+    acc = a.float() @ b.float()
+    out = torch.full((nb, M, N), 7.0, device="cuda", dtype=torch.bfloat16)
+    native.gemm(a, b, out)
+    assert rel_err(out, acc) < 1e-2
+    act = torch.full_like(out, 7.0)
+    native.gemm(a, b, out, epilogue=native.EPI_GELU_DUAL, aux=act)
+    assert rel_err(out, acc) < 1e-2
+    assert rel_err(act, torch.nn.functional.gelu(acc, approximate="tanh")) < 1e-2
+    aux = rnd(nb, M, N)
+    native.gemm(a, b, out, epilogue=native.EPI_ADD, aux=aux)
+    assert rel_err(out, acc + aux.float()) < 1e-2
+    # an output view inside a wider buffer: stores must stay within the view
+    big = torch.full((nb, M, N + 64), 5.0, device="cuda", dtype=torch.bfloat16)
+    native.gemm(a, b, big[..., :N])
+    assert rel_err(big[..., :N], acc) < 1e-2
+    assert bool((big[..., N:] == 5.0).all())
