@@ -44,6 +44,7 @@ struct GemmParams {
                       // block to a TMA bulk reduce-add (L2 does the read-modify-write)
   int aux_tma;        // 2-CTA kernel, epilogues 2/3: the aux block of the next 32-column chunk
                       // is TMA-loaded into the warp's staging buffer ahead of its use
+  int aux_db;         // 2-CTA kernel, aux_tma without c_tma: two aux buffers per warp
   int c_tma;          // 2-CTA kernel, bf16 C (and the epilogue-4 aux output): each 32 x 32
                       // chunk is staged in shared memory (64B swizzle) and written by a TMA
                       // tensor store, so C leaves the SM as whole lines, not 16B row pieces
@@ -365,7 +366,7 @@ struct Gemm2Cfg {
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int EPI_STAGE = kEpiWarps * 32 * 16 * 4;   // 32 rows x 16 fp32 per warp
   // [stages][epi staging][C store staging][barriers]; both staging areas 1024B aligned
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2 * EPI_STAGE + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2 * EPI_STAGE + 512;
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -541,7 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint64_t* aux_bar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kEpiWarps]
+  uint64_t* aux_bar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [2 * kEpiWarps]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -559,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * kEpiWarps);
     }
-    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -659,7 +660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
-    uint32_t aux_phase = 0;
+    uint32_t aux_phase = 0;   // bit b: phase of the warp's aux buffer b
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = pair; t < p.num_tiles; t += npairs) {
@@ -672,9 +673,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint16_t* ast = reinterpret_cast<uint16_t*>(epi_stage + (warp - 2) * 2048);   // 32 x 32 bf16
       uint8_t* cst = cst_stage + (warp - 2) * 2048;                                 // 32 x 32 bf16
       const bool warp_live = (m - lane) < p.M;
-      if (p.aux_tma && lane == 0) {        // first chunk's aux, under the mainloop's tail
-        mbar_arrive_expect_tx(&aux_bar[warp - 2], 2048);
-        tma_load_4d(&tmX, &aux_bar[warp - 2], ast, tl.n0 + c_lo * 32, m - lane, b1, b0);
+      // aux chunks (64B-swizzled, like the C staging): buffer 0 = ast, buffer 1 = cst when
+      // C leaves by direct stores (aux_db), so the loads run two chunks ahead
+      uint64_t* abar = aux_bar + 2 * (warp - 2);
+      if (p.aux_tma && lane == 0) {        // first chunks' aux, under the mainloop's tail
+        mbar_arrive_expect_tx(&abar[0], 2048);
+        tma_load_4d(&tmX, &abar[0], reinterpret_cast<uint8_t*>(ast), tl.n0 + c_lo * 32, m - lane, b1, b0);
+        if (p.aux_db && c_lo + 1 < c_hi) {
+          mbar_arrive_expect_tx(&abar[1], 2048);
+          tma_load_4d(&tmX, &abar[1], cst, tl.n0 + (c_lo + 1) * 32, m - lane, b1, b0);
+        }
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -685,13 +693,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         const int n = tl.n0 + c * 32;
         if (p.aux_tma) {
-          mbar_wait(&aux_bar[warp - 2], aux_phase);
-          aux_phase ^= 1;
+          const int ab = p.aux_db ? ((c - c_lo) & 1) : 0;
+          mbar_wait(&abar[ab], (aux_phase >> ab) & 1);
+          aux_phase ^= 1u << ab;
           float a[32];
-          const uint4* src = reinterpret_cast<const uint4*>(ast + lane * 32);
+          const uint4* src = reinterpret_cast<const uint4*>((ab ? cst : reinterpret_cast<uint8_t*>(ast)) + lane * 64);
+          const int sw = (lane >> 1) & 3;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const uint4 u = src[i];
+            const uint4 u = src[i ^ sw];
             const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -700,9 +710,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
           __syncwarp();                      // buffer read by every lane: refill it
-          if (c + 1 < c_hi && lane == 0) {
-            mbar_arrive_expect_tx(&aux_bar[warp - 2], 2048);
-            tma_load_4d(&tmX, &aux_bar[warp - 2], ast, n + 32, m - lane, b1, b0);
+          const int cn = c + 1 + p.aux_db;
+          if (cn < c_hi && lane == 0) {
+            mbar_arrive_expect_tx(&abar[ab], 2048);
+            tma_load_4d(&tmX, &abar[ab], (ab ? cst : reinterpret_cast<uint8_t*>(ast)), tl.n0 + cn * 32, m - lane, b1, b0);
           }
           if (p.c_tma) {
             if (warp_live && n < p.N)
@@ -1091,18 +1102,20 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
   p.aux_tma = 0;
   if (two_sm && (epilogue == 2 || epilogue == 3) && !no_aux_tma) {
     rc = make_map_box(&mx, aux, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, M, aux_desc[0], nbatch1,
-                      aux_desc[2], nbatch0, aux_desc[1], 32);
+                      aux_desc[2], nbatch0, aux_desc[1], 32, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
     p.aux_tma = 1;
   }
   // bf16 C (+ the dual epilogue's aux output) by TMA stores from swizzled staging;
   // operands whose strides a tensor map cannot describe keep the direct stores
   static const bool no_c_tma = getenv("MPEXEC_GEMM_NO_C_TMA") != nullptr;
+  static const bool aux_direct = getenv("MPEXEC_GEMM_AUX_DIRECT") != nullptr;
   p.c_tma = 0;
   // (aux-reading epilogues only unbatched: on the batched MoE expert GEMMs at K = 1024
   // the staged GeLU' path measured 20% slower than direct stores, 616 vs 769 TF/s)
   if (two_sm && c_dtype == 0 && beta == 0.f && !no_c_tma &&
-      (epilogue == 0 || epilogue == 1 || epilogue == 4 || (p.aux_tma && nbatch0 * nbatch1 == 1))) {
+      (epilogue == 0 || epilogue == 1 || epilogue == 4 ||
+       (p.aux_tma && nbatch0 * nbatch1 == 1 && !aux_direct))) {
     CUtensorMap mc2, mx2 = mx;
     int rc2 = make_map_box(&mc2, C, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, M, cd[2], nbatch1,
                            cd[5], nbatch0, cd[4], 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -1118,6 +1131,8 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
       clear_error();
     }
   }
+  static const bool no_aux_db = getenv("MPEXEC_GEMM_NO_AUX_DB") != nullptr;
+  p.aux_db = (p.aux_tma && !p.c_tma && !no_aux_db) ? 1 : 0;
   if (two_sm)
     rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, mbn, mc, mx, p, s)
                      : launch_gemm_2sm<128>(ma, mb, mbn, mc, mx, p, s);

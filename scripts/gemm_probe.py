@@ -56,11 +56,13 @@ CASES = [  # batch, M, N, K, ta, tb, f32 (beta=1 accumulate), epilogue
     (1, 8192, 8192, 2048, 0, 0, 0, 0), (1, 8192, 8192, 2048, 0, 0, 1, 0),
     (1, 8192, 8192, 2048, 0, 0, 0, 4), (1, 8192, 8192, 2048, 0, 1, 0, 3),
     (1, 2048, 2048, 8192, 1, 0, 1, 0),
+    (1, 8192, 2048, 2048, 0, 0, 0, 2), (1, 8192, 2048, 8192, 0, 0, 0, 2),
+    (16, 1024, 1024, 8192, 0, 0, 0, 2),
 ]
 for batch, M, N, K, ta, tb, f32, epi in CASES:
     a, b, out = mk(batch, M, N, K, ta, tb, f32)
     aux = torch.empty_like(out, dtype=torch.bfloat16) if epi else None
-    if epi == 3:
+    if epi in (2, 3):
         aux.normal_()
     fl = 2.0 * batch * M * N * K
     res = []
