@@ -198,4 +198,52 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x2);
 }
 
+// Packed fp32 pairs (Blackwell FFMA2 / FMUL2): the GEMM epilogues' GeLU and GeLU'
+// on two columns per instruction.  Same tanh formulation as gelu_tanh /
+// gelu_tanh_grad, re-associated (results agree to fp32 rounding).
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ uint64_t fma_x2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul_x2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// (gelu(x0), gelu(x1)): u = x (k0 + k0 k1 x^2), y = x/2 + x/2 tanh(u)
+__device__ __forceinline__ float2 gelu_tanh2(float x0, float x1) {
+  const float k0 = 0.7978845608028654f, k01 = 0.7978845608028654f * 0.044715f;
+  const uint64_t x = pk2(x0, x1), xx = mul_x2(x, x);
+  const float2 u = upk2(mul_x2(x, fma_x2(xx, pk2(k01, k01), pk2(k0, k0))));
+  const uint64_t t = pk2(tanh_fast(u.x), tanh_fast(u.y));
+  const uint64_t hx = mul_x2(x, pk2(0.5f, 0.5f));
+  return upk2(fma_x2(hx, t, hx));
+}
+// (g0 gelu'(x0), g1 gelu'(x1)) with h = x (k0/2 + 3/2 k0 k1 x^2):
+// gelu'(x) = 1/2 + 1/2 t + h (1 - t^2) = 1/2 + t (1/2 - h t) + h.  |x| is clamped to
+// 16, where tanh has saturated (gelu' = 0 or 1) and x^3 cannot overflow.
+__device__ __forceinline__ float2 gelu_grad_mul2(float g0, float g1, float x0, float x1) {
+  const float k0 = 0.7978845608028654f, k01 = 0.7978845608028654f * 0.044715f;
+  const uint64_t x = pk2(fminf(fmaxf(x0, -16.f), 16.f), fminf(fmaxf(x1, -16.f), 16.f));
+  const uint64_t xx = mul_x2(x, x);
+  const float2 u = upk2(mul_x2(x, fma_x2(xx, pk2(k01, k01), pk2(k0, k0))));
+  const uint64_t t = pk2(tanh_fast(u.x), tanh_fast(u.y));
+  const uint64_t nh = mul_x2(x, fma_x2(xx, pk2(-1.5f * k01, -1.5f * k01), pk2(-0.5f * k0, -0.5f * k0)));
+  const uint64_t half = pk2(0.5f, 0.5f);
+  const uint64_t a2 = fma_x2(t, fma_x2(nh, t, half), half);
+  const uint64_t gp = fma_x2(nh, pk2(-1.f, -1.f), a2);
+  return upk2(mul_x2(pk2(g0, g1), gp));
+}
+
 }  // namespace mp

@@ -86,19 +86,26 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
   if (p.epi == 1) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+    for (int i = 0; i < 32; i += 2) {
+      const float2 y = gelu_tanh2(v[i], v[i + 1]);
+      v[i] = y.x;
+      v[i + 1] = y.y;
+    }
   } else if (p.epi >= 2) {
     uint16_t* ax = p.aux + (int64_t)b0 * p.aux_bs0 + (int64_t)b1 * p.aux_bs1 +
                    (int64_t)m * p.aux_ld + n;
     if (p.epi == 4) {      // dual output: aux <- gelu(pre), C <- pre
       if (n + 32 <= p.N) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          reinterpret_cast<uint4*>(ax)[i] = make_uint4(
-              pack_bf2(gelu_tanh(v[8 * i]), gelu_tanh(v[8 * i + 1])),
-              pack_bf2(gelu_tanh(v[8 * i + 2]), gelu_tanh(v[8 * i + 3])),
-              pack_bf2(gelu_tanh(v[8 * i + 4]), gelu_tanh(v[8 * i + 5])),
-              pack_bf2(gelu_tanh(v[8 * i + 6]), gelu_tanh(v[8 * i + 7])));
+        for (int i = 0; i < 4; ++i) {
+          uint32_t w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 y = gelu_tanh2(v[8 * i + 2 * j], v[8 * i + 2 * j + 1]);
+            w[j] = pack_bf2(y.x, y.y);
+          }
+          reinterpret_cast<uint4*>(ax)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -129,7 +136,11 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t row_off
         for (int i = 0; i < 32; ++i) v[i] += a[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] *= gelu_tanh_grad(a[i]);
+        for (int i = 0; i < 32; i += 2) {
+          const float2 y = gelu_grad_mul2(v[i], v[i + 1], a[i], a[i + 1]);
+          v[i] = y.x;
+          v[i + 1] = y.y;
+        }
       }
     }
   }
@@ -466,13 +477,21 @@ __device__ __forceinline__ void tma_store_chunk(const GemmParams& p, const uint3
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
   if (p.epi == 1) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+    for (int i = 0; i < 32; i += 2) {
+      const float2 y = gelu_tanh2(v[i], v[i + 1]);
+      v[i] = y.x;
+      v[i + 1] = y.y;
+    }
   } else if (p.epi == 2) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] += apre[i];
   } else if (p.epi == 3) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= gelu_tanh_grad(apre[i]);
+    for (int i = 0; i < 32; i += 2) {
+      const float2 y = gelu_grad_mul2(v[i], v[i + 1], apre[i], apre[i + 1]);
+      v[i] = y.x;
+      v[i + 1] = y.y;
+    }
   }
   if (lane == 0) bulk_wait_read_g();
   __syncwarp();
@@ -486,11 +505,15 @@ __device__ __forceinline__ void tma_store_chunk(const GemmParams& p, const uint3
   if (p.epi == 4) {
     uint4* xrow = reinterpret_cast<uint4*>(xst + lane * 64);
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      xrow[j ^ sw] = make_uint4(pack_bf2(gelu_tanh(v[8 * j]), gelu_tanh(v[8 * j + 1])),
-                                pack_bf2(gelu_tanh(v[8 * j + 2]), gelu_tanh(v[8 * j + 3])),
-                                pack_bf2(gelu_tanh(v[8 * j + 4]), gelu_tanh(v[8 * j + 5])),
-                                pack_bf2(gelu_tanh(v[8 * j + 6]), gelu_tanh(v[8 * j + 7])));
+    for (int j = 0; j < 4; ++j) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 y = gelu_tanh2(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+        w[e] = pack_bf2(y.x, y.y);
+      }
+      xrow[j ^ sw] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
   fence_proxy_async_smem();
   __syncwarp();

@@ -273,3 +273,24 @@ def test_gemm_fused_epilogues_batched(nb, M, N, K):
     native.gemm(a, b, big[..., :N])
     assert rel_err(big[..., :N], acc) < 1e-2
     assert bool((big[..., N:] == 5.0).all())
+
+
+@pytest.mark.parametrize("nb", [1, 4])
+def test_gemm_gelu_epilogues_wide_range(nb):
+    """Packed-pair GeLU / GeLU' epilogues over pre-activations far into both
+    saturated tails (|x| up to 40, past the clamp at 16) against torch fp32."""
+    M, N, K = 512, 512, 128
+    a, b = rnd(nb, M, K), rnd(nb, K, N, scale=0.1)
+    acc = a.float() @ b.float()
+    pre = (torch.rand(nb, M, N, device="cuda") * 80 - 40).to(torch.bfloat16)
+    out = torch.empty(nb, M, N, device="cuda", dtype=torch.bfloat16)
+    native.gemm(a, b, out, epilogue=native.EPI_GELU_GRAD, aux=pre)
+    xf = pre.float().requires_grad_()
+    torch.nn.functional.gelu(xf, approximate="tanh").backward(acc)
+    assert rel_err(out, xf.grad) < 1e-2
+    assert torch.isfinite(out.float()).all()
+    big = torch.empty_like(out)
+    a2 = rnd(nb, M, K, scale=8.0)
+    acc2 = a2.float() @ b.float()
+    native.gemm(a2, b, out, epilogue=native.EPI_GELU_DUAL, aux=big)
+    assert rel_err(big, torch.nn.functional.gelu(acc2, approximate="tanh")) < 1e-2
