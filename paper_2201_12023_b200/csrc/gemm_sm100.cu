@@ -473,8 +473,13 @@ __device__ __forceinline__ void tma_store_chunk(const GemmParams& p, const uint3
                                                 int n, int m0, int b0, int b1) {
   const int lane = threadIdx.x & 31;
   float v[32];
+  const uint64_t al = pk2(p.alpha, p.alpha);
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+  for (int i = 0; i < 32; i += 2) {
+    const float2 y = upk2(mul_x2(pk2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), al));
+    v[i] = y.x;
+    v[i + 1] = y.y;
+  }
   if (p.epi == 1) {
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
@@ -484,7 +489,11 @@ __device__ __forceinline__ void tma_store_chunk(const GemmParams& p, const uint3
     }
   } else if (p.epi == 2) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] += apre[i];
+    for (int i = 0; i < 32; i += 2) {
+      const float2 y = upk2(add_x2(pk2(v[i], v[i + 1]), pk2(apre[i], apre[i + 1])));
+      v[i] = y.x;
+      v[i + 1] = y.y;
+    }
   } else if (p.epi == 3) {
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
