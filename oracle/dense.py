@@ -12,13 +12,15 @@ from . import ir
 
 def gelu(x):
     k0, k1 = 0.7978845608028654, 0.044715
-    return 0.5 * x * (1.0 + np.tanh(k0 * (x + k1 * x ** 3)))
+    x2 = x * x
+    return 0.5 * x * (1.0 + np.tanh(k0 * x * (1.0 + k1 * x2)))
 
 
 def gelu_grad(x):
     k0, k1 = 0.7978845608028654, 0.044715
-    t = np.tanh(k0 * (x + k1 * x ** 3))
-    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * k0 * (1 + 3 * k1 * x * x)
+    x2 = x * x
+    t = np.tanh(k0 * x * (1.0 + k1 * x2))
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * k0 * (1 + 3 * k1 * x2)
 
 
 def softmax(x, scale):

@@ -238,9 +238,15 @@ __device__ __forceinline__ float2 gelu_tanh2(float x0, float x1) {
 // (g0 gelu'(x0), g1 gelu'(x1)) with h = x (k0/2 + 3/2 k0 k1 x^2):
 // gelu'(x) = 1/2 + 1/2 t + h (1 - t^2) = 1/2 + t (1/2 - h t) + h.  |x| is clamped to
 // 16, where tanh has saturated (gelu' = 0 or 1) and x^3 cannot overflow.
+// The clamp propagates NaN (min/max.NaN), like the unfused gelu_tanh_grad does.
+__device__ __forceinline__ float clamp16_nan(float x) {
+  float r;
+  asm("max.NaN.f32 %0, %1, 0fC1800000;\n\tmin.NaN.f32 %0, %0, 0f41800000;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float2 gelu_grad_mul2(float g0, float g1, float x0, float x1) {
   const float k0 = 0.7978845608028654f, k01 = 0.7978845608028654f * 0.044715f;
-  const uint64_t x = pk2(fminf(fmaxf(x0, -16.f), 16.f), fminf(fmaxf(x1, -16.f), 16.f));
+  const uint64_t x = pk2(clamp16_nan(x0), clamp16_nan(x1));
   const uint64_t xx = mul_x2(x, x);
   const float2 u = upk2(mul_x2(x, fma_x2(xx, pk2(k01, k01), pk2(k0, k0))));
   const uint64_t t = pk2(tanh_fast(u.x), tanh_fast(u.y));

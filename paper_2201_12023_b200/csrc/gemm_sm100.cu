@@ -1035,6 +1035,13 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
   MP_CHECK_ARG(nbatch0 >= 1 && nbatch1 >= 1, "bad batch extents");
   MP_CHECK_ARG(reinterpret_cast<uintptr_t>(C) % 16 == 0 && cd[2] % (c_dtype ? 4 : 8) == 0,
                "C must be 16-byte aligned with 16-byte aligned rows");
+  // the epilogue's 16-byte C / aux accesses start at every batch's base too
+  MP_CHECK_ARG((nbatch0 == 1 || cd[4] % (c_dtype ? 4 : 8) == 0) &&
+                   (nbatch1 == 1 || cd[5] % (c_dtype ? 4 : 8) == 0),
+               "C batch strides must be 16-byte multiples");
+  MP_CHECK_ARG(epilogue < 2 || ((nbatch0 == 1 || aux_desc[1] % 8 == 0) &&
+                                (nbatch1 == 1 || aux_desc[2] % 8 == 0)),
+               "aux batch strides must be 16-byte multiples");
 
   GemmParams p{};
   p.M = (int)M;

@@ -203,7 +203,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, alpha: float = 
         if xb != cb or xd[0] != cd[0] or xd[1] != cd[1] or xd[3] != 1:
             raise NativeError("aux must match out's shape with unit column stride")
         aux_ptr, aux_desc = aux.data_ptr(), _arr([xd[2], xd[4], xd[5]])
-    if epi == 0 and beta != 0.0 and out.dtype == torch.float32 and a.dim() == 2 and \
+    if epi == 0 and out.dtype == torch.float32 and a.dim() == 2 and \
             b.dim() == 2 and out.is_contiguous():
         s = _split_k(ad[0], bd[1], ad[1])
         if s > 1:

@@ -22,6 +22,7 @@ from __future__ import annotations
 import math
 import os
 import time
+import zlib
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -38,6 +39,12 @@ from .plan import (KIND_PARAM, ExecPlan, Mesh, PlanError, Spec, box_numel, devic
                    local_dims, replicated)
 from .schedule import GPIPE, Instr, Program, build_program, modeled_makespan
 from .xmesh import recvs_of, sends_of
+
+
+def stable_seed(*parts) -> int:
+    """Process-independent 31-bit seed (Python's str hash is salted per process,
+    so hash() would give every torchrun rank different synthetic weights)."""
+    return zlib.crc32("/".join(str(p) for p in parts).encode()) & 0x7FFFFFFF
 
 
 class ExecError(RuntimeError):
@@ -148,6 +155,7 @@ class StageRunner:
         self.dw_stream = (torch.cuda.Stream() if os.environ.get("MPEXEC_DW_STREAM", "1") != "0"
                           else None)
         self.dw_pending = False
+        self.g_fresh: set[int] = set()
         self._compile()
         self._init_params(params)
         self.step_count = 0
@@ -172,6 +180,7 @@ class StageRunner:
         self.cap_vals: dict = {}
         self.cap_aux: dict = {}
         self.static: dict = {}
+        self.slot_send_ev: dict[int, torch.cuda.Event] = {}
 
         self.input_mode = "host" if host_inputs else ("fn" if inputs is not None else "resident")
         self._resident_inputs: dict = {}
@@ -615,6 +624,10 @@ class StageRunner:
         dv = torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev)
         native.attn_bwd(q, k, v, o, dout, lse, dvec, dq_acc, dk, dv, Bl, Hl, s, d, cl["scale"],
                         kv_range=(k0, k1 - k0))
+        axes = cl["key_axes"] if cl["local"] is None else ()
+        if axes:
+            # sum the fp32 partials across the key groups, round to bf16 once
+            self._allreduce(dq_acc, axes)
         dq = native.cast_f32_bf16(dq_acc, torch.empty(T, hdim, dtype=torch.bfloat16, device=self.dev))
         if cl["local"] is not None:
             for n, t in ((cl["dqh"], dq), (cl["dkh"], dk), (cl["dvh"], dv)):
@@ -622,9 +635,7 @@ class StageRunner:
                 vals[m] = (self._coerce(t, g[m].dims, L, self.spec(m)) if m in self.out_ids
                            else t)
             return None
-        axes = cl["key_axes"]
         if axes:
-            self._allreduce(dq, axes)
             ks = Spec(((), (), axes))
             vs = Spec(((), axes, ()))
         else:
@@ -749,7 +760,7 @@ class StageRunner:
                 full_init[off:off + sz].copy_(torch.from_numpy(np.ascontiguousarray(loc)).reshape(-1))
             else:
                 gen = torch.Generator(device=self.dev)
-                gen.manual_seed(hash((self.seed, "param", pid)) & 0x7FFFFFFF)
+                gen.manual_seed(stable_seed(self.seed, "param", pid))
                 # GPT-style init (std 0.02) keeps the 24-block residual stream O(1)
                 full = torch.randn(g[pid].dims, generator=gen, device=self.dev) * self.init_std
                 loc = full[tuple(slice(lo, hi) for lo, hi in box)]
@@ -924,13 +935,19 @@ class StageRunner:
             # overlaps the dX chain and fills the other GEMMs' tail waves
             gv = self.gviews[op.nid]
             out_view = gv if a.dim() == 2 else gv.view(*a.shape[:-2], a.shape[-2], b.shape[-1])
+            # the step's first contribution overwrites (beta = 0): no zero fill
+            # of the fp32 gradient buffers between steps
+            beta = 1.0
+            if op.nid in self.g_fresh:
+                self.g_fresh.discard(op.nid)
+                beta = 0.0
             main = torch.cuda.current_stream()
             if self.dw_stream is None:
-                self._gemm(a, b, out_view, beta=1.0)
+                self._gemm(a, b, out_view, beta=beta)
                 return None
             self.dw_stream.wait_stream(main)
             with torch.cuda.stream(self.dw_stream):
-                self._gemm(a, b, out_view, beta=1.0)
+                self._gemm(a, b, out_view, beta=beta)
             a.record_stream(self.dw_stream)
             b.record_stream(self.dw_stream)
             self.dw_pending = True
@@ -1121,7 +1138,7 @@ class StageRunner:
             hb = self._host_input_bufs.get(key)
             if hb is None:
                 gen = torch.Generator()
-                gen.manual_seed(hash((self.seed, "input", op.nid, mb % 2)) & 0x7FFFFFFF)
+                gen.manual_seed(stable_seed(self.seed, "input", op.nid, mb % 2))
                 full = torch.randn(dims, generator=gen)
                 hb = full[sl].contiguous().to(torch.bfloat16).pin_memory()
                 self._host_input_bufs[key] = hb
@@ -1130,7 +1147,7 @@ class StageRunner:
         t = self._resident_inputs.get(key)
         if t is None:
             gen = torch.Generator(device=self.dev)
-            gen.manual_seed(hash((self.seed, "input", op.nid, mb % 2)) & 0x7FFFFFFF)
+            gen.manual_seed(stable_seed(self.seed, "input", op.nid, mb % 2))
             full = torch.randn(dims, generator=gen, device=self.dev, dtype=torch.float32)
             t = full[sl].to(torch.bfloat16).contiguous()
             self._resident_inputs[key] = t
@@ -1140,6 +1157,14 @@ class StageRunner:
     # ------------------------------------------------------------------ CUDA graphs
     def slot_of(self, mb: int) -> int:
         return mb % self.n_slots
+
+    def _slot_guard(self, mb: int) -> None:
+        """Graph mode: a slot's static buffers (captured outputs, staged inputs,
+        received tensors) are rewritten when the slot is reused for microbatch
+        mb; the compute stream first waits for the last send that read them."""
+        ev = self.slot_send_ev.pop(self.slot_of(mb), None)
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
 
     def _graph_inputs(self, mb: int):
         """Graph mode: stage this microbatch's graph inputs into the slot's
@@ -1165,6 +1190,7 @@ class StageRunner:
         are never live for two microbatches at once."""
         if not self.use_graphs:
             return self._compute_eager(phase, mb)
+        self._slot_guard(mb)
         if phase == "fwd":
             self._graph_inputs(mb)
         key = (phase, self.slot_of(mb))
@@ -1227,6 +1253,7 @@ class StageRunner:
             dspec = canonical(bt.dst_spec, self.mesh)
             shape = local_dims(node.dims, dspec, self.mesh)
             if self.use_graphs:
+                self._slot_guard(mb)
                 key = ("recv", self.slot_of(mb), bt.node)
                 out = self.static.get(key)
                 if out is None:
@@ -1315,6 +1342,12 @@ class StageRunner:
                           stream=self.send_stream)
             for buf, _ in sends:
                 buf.record_stream(self.send_stream)
+            if self.use_graphs:
+                # record_stream does not protect graph-pool memory: the slot's
+                # next replay waits on this event instead (_slot_guard)
+                ev = torch.cuda.Event()
+                ev.record(self.send_stream)
+                self.slot_send_ev[self.slot_of(mb)] = ev
             self.sends_pending = True
 
     def free(self, ins: Instr):
@@ -1403,6 +1436,13 @@ class StageRunner:
 
     def zero_grads(self):
         self.join_dw()
+        if not self.use_graphs:
+            # every dW GEMM's first launch of the step runs with beta = 0; the
+            # gradbuf regions no dW writes stay at their initial zeros
+            self.g_fresh = set(self.gviews)
+            return
+        # a captured backward replays one fixed beta: keep the explicit fill
+        self.g_fresh = set()
         self.gradbuf.zero_()
         for dw, gv in self.gviews.items():
             if gv.data_ptr() < self.gradbuf.data_ptr() or \

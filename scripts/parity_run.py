@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--train-steps", type=int, default=0,
                     help="instead of the oracle check: run N steps with Adam updates and "
                          "print the per-step losses (used to compare optimizer paths)")
+    ap.add_argument("--no-oracle", action="store_true",
+                    help="with --train-steps: skip the oracle's training run")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
@@ -32,9 +34,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.train_steps:
         from parity_harness import train_losses
-        losses = train_losses(args.plan, args.schedule, args.train_steps)
-        if losses is not None:
-            print(json.dumps({"losses": losses, "plan": args.plan}), flush=True)
+        res = train_losses(args.plan, args.schedule, args.train_steps,
+                           oracle=not args.no_oracle)
+        if res is not None:
+            res["plan"] = args.plan
+            print(json.dumps(res), flush=True)
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()

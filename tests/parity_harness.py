@@ -44,15 +44,18 @@ def synth(doc: dict, seed: int = 0):
     gain = 1.0 if blocks <= 2 else 1.0 / np.sqrt(blocks)
     # scale by the contraction length (dims[-2]: rows of a 2-D weight, the
     # per-expert fan-in of a 3-D MoE expert weight)
-    params = {n["id"]: (rng.standard_normal(n["shape"]["dims"]) * gain /
-                        np.sqrt(n["shape"]["dims"][-2]))
-              .astype(np.float32) for n in nodes if n["kind"] == "parameter"}
+    params = {}
+    for n in nodes:
+        if n["kind"] == "parameter":
+            w = rng.standard_normal(n["shape"]["dims"], dtype=np.float32)
+            w *= np.float32(gain / np.sqrt(n["shape"]["dims"][-2]))
+            params[n["id"]] = w
     cache = {}
 
     def inputs(mb, nid):
         if (mb, nid) not in cache:
             r = np.random.default_rng(1000 * (seed + 1) + 7 * mb + nid)
-            cache[(mb, nid)] = r.standard_normal(nodes[nid]["shape"]["dims"]).astype(np.float32)
+            cache[(mb, nid)] = r.standard_normal(nodes[nid]["shape"]["dims"], dtype=np.float32)
         return cache[(mb, nid)]
     return params, inputs
 
@@ -85,7 +88,7 @@ def routing_margin(doc, params, inputs) -> float:
     return m
 
 
-def bf16_storage_errors(doc, p16, x16, routes, L, G, O) -> dict:
+def bf16_storage_errors(doc, p16, x16, routes, L, G, O, dtype=np.float64) -> dict:
     """Errors of the float64 oracle with every node's value rounded to bf16 (what
     bf16 activation storage alone costs on this graph), against the plain oracle."""
     from oracle import dense
@@ -93,10 +96,10 @@ def bf16_storage_errors(doc, p16, x16, routes, L, G, O) -> dict:
 
     def rounded(*a, **k):
         r = orig(*a, **k)
-        return bf16_round(r).astype(np.float64) if isinstance(r, np.ndarray) else r
+        return bf16_round(r).astype(dtype) if isinstance(r, np.ndarray) else r
     dense.eval_node = rounded
     try:
-        L2, G2, O2 = dense.run(doc, p16, x16, doc["num_microbatches"], routes=routes)
+        L2, G2, O2 = dense.run(doc, p16, x16, doc["num_microbatches"], routes=routes, dtype=dtype)
     finally:
         dense.eval_node = orig
     out = {"loss": abs(L2 - L) / abs(L), "grad": max((rel(G2[k], G[k]) for k in G), default=0.0),
@@ -115,13 +118,18 @@ def rel(a, b):
 
 def bf16_round(x):
     """Round fp32 values to bf16 (what the GPU sees of the same inputs)."""
-    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
-    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
-    return u.astype(np.uint32).view(np.float32)
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32)
+    r = (u >> 16) & np.uint32(1)
+    r += np.uint32(0x7FFF)
+    r += u                      # wraps only for NaN payloads
+    r &= np.uint32(0xFFFF0000)
+    return r.view(np.float32)
 
 
-def compare(doc, result, params, inputs):
-    """Oracle (dense float64 on bf16-rounded inputs) vs the executor result."""
+def compare(doc, result, params, inputs, dtype=np.float64):
+    """Oracle (dense float64 on bf16-rounded inputs) vs the executor result.
+    dtype=np.float32 for the full-size plans (fp32 accumulation error ~1e-6,
+    three orders below the bf16 tolerances; half the oracle's time and memory)."""
     from oracle import dense
     p16 = {k: bf16_round(v) for k, v in params.items()}
     x16 = lambda mb, nid: bf16_round(inputs(mb, nid))  # noqa: E731
@@ -132,7 +140,7 @@ def compare(doc, result, params, inputs):
         # oracle's on every token whose top-3 logit gaps exceed ROUTE_TIE; the
         # numerics are then compared with the GPU's decisions replayed.
         trace = {g: [] for g in gate_nodes(doc)}
-        dense.run(doc, p16, x16, doc["num_microbatches"], trace=trace)
+        dense.run(doc, p16, x16, doc["num_microbatches"], trace=trace, dtype=dtype)
         mism = ties = 0
         for (mb, gid), tab in routes.items():
             lg = np.log(np.maximum(trace[gid][mb], 1e-300))
@@ -144,10 +152,10 @@ def compare(doc, result, params, inputs):
             ties += int((~clear).sum())
             mism += int(((order[:, 0] != tab[:, 0]) | (order[:, 1] != tab[:, 2]))[clear].sum())
         route_errs = {"route_mismatch": mism, "route_near_ties": ties}
-    L, G, O = dense.run(doc, p16, x16, doc["num_microbatches"], routes=routes)
+    L, G, O = dense.run(doc, p16, x16, doc["num_microbatches"], routes=routes, dtype=dtype)
     errs = {"loss": abs(result.loss - L) / abs(L), "oracle_loss": L, "gpu_loss": result.loss}
     errs.update(route_errs)
-    emu = bf16_storage_errors(doc, p16, x16, routes, L, G, O)
+    emu = bf16_storage_errors(doc, p16, x16, routes, L, G, O, dtype)
     errs["bf16_storage"] = emu
     per = {k: rel(result.grads[k], G[k]) for k in G}
     errs["grad"] = max(per.values()) if per else 0.0
@@ -171,7 +179,7 @@ def compare(doc, result, params, inputs):
     return errs
 
 
-def run_plan(plan_path, schedule="1f1b", seed=0):
+def run_plan(plan_path, schedule="1f1b", seed=0, dtype=np.float64):
     """Execute one step (collect grads, no update) on this process group and
     compare on rank 0.  Returns the error dict (rank 0) or None."""
     import torch.distributed as dist
@@ -183,25 +191,42 @@ def run_plan(plan_path, schedule="1f1b", seed=0):
     rank = dist.get_rank() if dist.is_initialized() else 0
     if rank != 0:
         return None
-    errs = compare(doc, res, params, inputs)
+    errs = compare(doc, res, params, inputs, dtype=dtype)
     errs["gpu_launches"] = res.gpu_launches
     errs["makespan_s"] = res.makespan
     errs["fused"] = res.fused
     return errs
 
 
-def train_losses(plan_path, schedule="1f1b", steps=3, seed=0):
-    """Losses of `steps` training steps (Adam updates between them) on this
-    process group; rank 0 returns them, other ranks None."""
+TRAIN_LR = 1e-3     # large enough that three Adam steps move the loss visibly
+
+
+def train_losses(plan_path, schedule="1f1b", steps=3, seed=0, oracle=True, lr=TRAIN_LR):
+    """`steps` training steps (Adam updates between them) on this process group.
+    Rank 0 returns {"losses": executor losses, "oracle": the oracle's
+    (oracle/adam.py: same update rule, fp32 master, bf16 working weights),
+    "err": max relative loss error, "zero_params": parameters under the ZeRO
+    rewrite on rank 0}; other ranks None."""
     import torch.distributed as dist
-    from paper_2201_12023_b200.runtime import Executor
+    from paper_2201_12023_b200.runtime import AdamConfig, Executor
     doc = json.loads(Path(plan_path).read_text())
     params, inputs = synth(doc, seed)
-    ex = Executor(doc, schedule=schedule, params=params, inputs=inputs, seed=seed)
+    ex = Executor(doc, schedule=schedule, params=params, inputs=inputs, seed=seed,
+                  adam=AdamConfig(lr=lr))
     out = []
     for _ in range(steps):
         ex.barrier()
         ex.step()
         out.append(ex.loss())
     rank = dist.get_rank() if dist.is_initialized() else 0
-    return out if rank == 0 else None
+    if rank != 0:
+        return None
+    res = {"losses": out, "zero_params": len(ex.runner.zero)}
+    if oracle:
+        from oracle import adam
+        a = AdamConfig(lr=lr)
+        ref, _ = adam.train(doc, params, inputs, steps, lr=a.lr, beta1=a.beta1, beta2=a.beta2,
+                            eps=a.eps, weight_decay=a.weight_decay)
+        res["oracle"] = ref
+        res["err"] = max(abs(x - y) / abs(y) for x, y in zip(out, ref))
+    return res

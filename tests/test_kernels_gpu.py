@@ -294,3 +294,45 @@ def test_gemm_gelu_epilogues_wide_range(nb):
     acc2 = a2.float() @ b.float()
     native.gemm(a2, b, out, epilogue=native.EPI_GELU_DUAL, aux=big)
     assert rel_err(big, torch.nn.functional.gelu(acc2, approximate="tanh")) < 1e-2
+
+
+@pytest.mark.parametrize("nb", [1, 3])
+def test_gemm_gelu_grad_epilogue_propagates_nan(nb):
+    """A NaN pre-activation gives a NaN gradient in the fused GeLU' epilogue, as it
+    does in the unfused gelu_bwd kernel (the |x| <= 16 clamp is NaN-propagating)."""
+    M, N, K = 256, 512, 128
+    a, b = rnd(nb, M, K), rnd(nb, K, N, scale=0.1)
+    pre = rnd(nb, M, N)
+    pre[:, 3, 7] = float("nan")
+    pre[:, 100, 300] = float("inf")
+    out = torch.empty(nb, M, N, device="cuda", dtype=torch.bfloat16)
+    native.gemm(a, b, out, epilogue=native.EPI_GELU_GRAD, aux=pre)
+    assert bool(torch.isnan(out[:, 3, 7]).all())
+    fin = torch.isfinite(pre.float())
+    xf = pre.float().where(fin, torch.zeros_like(pre.float())).requires_grad_()
+    torch.nn.functional.gelu(xf, approximate="tanh").backward(a.float() @ b.float())
+    assert rel_err(out.float()[fin], xf.grad[fin]) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 8192), (2048, 2048, 1024)])
+def test_gemm_f32_overwrite_beta0(M, N, K):
+    """The step's first dW launch overwrites the fp32 gradient buffer (beta = 0,
+    no zero fill): garbage in C (NaN included) never leaks into the result, on the
+    split-K path and the plain kernel."""
+    a = rnd(K, M).t()
+    b = rnd(K, N)
+    out = torch.full((M, N), float("nan"), device="cuda")
+    native.gemm(a, b, out, beta=0.0)
+    assert rel_err(out, a.float() @ b.float()) < 2e-3
+
+
+def test_gemm_rejects_misaligned_batch_strides():
+    """16-byte C / aux accesses start at every batch base: an odd batch stride
+    is an argument error (rc 2), never a device fault."""
+    a, b = rnd(2, 256, 64), rnd(2, 64, 256)
+    buf = torch.empty(2 * 256 * 256 + 3, device="cuda", dtype=torch.bfloat16)
+    out = buf.as_strided((2, 256, 256), (256 * 256 + 3, 256, 1))
+    aux = rnd(2, 256, 256)
+    with pytest.raises(native.NativeError):
+        native.gemm(a, b, out, epilogue=native.EPI_ADD, aux=aux)
+    torch.cuda.synchronize()
