@@ -39,6 +39,10 @@ const char* mp_last_error(void);
 /* Number of device kernels this library has launched since load (all entry
  * points; used by bench.py for the `gpu_launches` claim). */
 uint64_t mp_launch_count(void);
+/* Load every libmpexec kernel now (CUDA lazy module loading would load a kernel at
+ * its first launch, blocking the host while an NCCL kernel spins on the device).
+ * Called once per process by the executor; 0 ok. */
+int mp_preload_kernels(void);
 
 /* ---- GEMM ------------------------------------------------------------------
  * Replaces the modeled local matmul of a chosen ParallelAlgorithm
@@ -195,6 +199,13 @@ int mp_nccl_version(void);
 int mp_nccl_unique_id(void* out128);
 int mp_comm_init(const void* uid128, int nranks, int rank, void** comm_out);
 int mp_comm_destroy(void* comm);
+/* Release a hung communicator (every pending operation on it fails) and poll a
+ * communicator's asynchronous error state without blocking; nccl_result gets the
+ * ncclResult_t (0 ok).  The executor's watchdog uses them to turn a hang into an
+ * ExecError naming the blocked instruction (the deadlock SimError of
+ * sim.py:172-178). */
+int mp_comm_abort(void* comm);
+int mp_comm_async_error(void* comm, int* nccl_result);
 int mp_allreduce(void* comm, void* buf, int64_t count, int dtype, int op, void* stream);
 int mp_allgather(void* comm, const void* send, void* recv, int64_t sendcount, int dtype,
                  void* stream);

@@ -19,6 +19,7 @@ Group ranks are ordered by global device id (= NCCL rank order).
 """
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass, field
 
 import torch
@@ -89,8 +90,27 @@ class Comm:
             g = self._groups[k]
             if rank in g.local:
                 g.comm = native.comm_init(ids[k], len(g.ranks), g.local[rank])
+        self._connect(uniq)
         # torch group for step-level reductions (loss, barrier, max time)
         self.world_group = dist.new_group(ranks=list(range(world)))
+
+    def _connect(self, keys) -> None:
+        """Establish every P2P connection up front: one all-pairs exchange of
+        one element per communicator, in the same global order on every rank.
+        NCCL connects peers lazily, and the lazy handshake blocks the host in
+        ncclGroupEnd until the peer posts its side; connected up front, a send
+        that never comes is a device-side wait the watchdog can see (and the
+        first timed step pays no connection setup)."""
+        buf = torch.zeros(2 * self.world, dtype=torch.float32, device="cuda")
+        for k in keys:
+            g = self._groups[k]
+            if self.rank not in g.local or len(g.ranks) < 2:
+                continue
+            me = g.local[self.rank]
+            peers = [i for i in range(len(g.ranks)) if i != me]
+            native.send_recv(g.comm, [(buf[i:i + 1], i) for i in peers],
+                             [(buf[self.world + i:self.world + i + 1], i) for i in peers])
+        torch.cuda.synchronize()
 
     def stage_group(self, st_index: int, mesh: Mesh) -> Group:
         return self._groups[("stage", st_index, tuple(sorted(mesh.device_ids)))]
@@ -126,6 +146,36 @@ class Comm:
     def reduce_scatter_into(self, out_flat: torch.Tensor, in_flat: torch.Tensor, group: Group,
                             stream=None) -> None:
         native.reduce_scatter(group.comm, out_flat, in_flat, stream)
+
+    def async_errors(self) -> list[str]:
+        """Groups whose communicator reports an asynchronous NCCL failure."""
+        bad = []
+        for k, g in self._groups.items():
+            if g.comm:
+                r = native.comm_async_error(g.comm)
+                if r not in (0, 7):                   # ncclSuccess, ncclInProgress
+                    bad.append(f"{k[0]} group {list(g.ranks)}: ncclResult {r}")
+        return bad
+
+    def abort(self, timeout: float = 60.0) -> bool:
+        """Release every pending operation (watchdog path); the communicators
+        are unusable afterwards.  All communicators are aborted concurrently:
+        ncclCommAbort frees device memory, which waits for the device, so
+        aborting an idle communicator while another one's kernel still spins
+        would block until that kernel is aborted too.  Returns False when an
+        abort has not returned within `timeout` seconds."""
+        import threading
+        comms = [g.comm for g in self._groups.values() if g.comm]
+        for g in self._groups.values():
+            g.comm = 0
+        threads = [threading.Thread(target=native.comm_abort, args=(c,), daemon=True)
+                   for c in comms]
+        for t in threads:
+            t.start()
+        end = time.monotonic() + timeout
+        for t in threads:
+            t.join(max(0.0, end - time.monotonic()))
+        return not any(t.is_alive() for t in threads)
 
     def close(self) -> None:
         for g in self._groups.values():

@@ -899,6 +899,19 @@ static bool fa_args_ok(const void* p, int64_t ld) {
   return p && (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld % 8 == 0);
 }
 
+
+// Force-load this file's kernels (lazy module loading would load a kernel at its
+// first launch, which blocks the host while an NCCL kernel spins on the device:
+// a deadlock the executor's watchdog could not see).  See mp_preload_kernels.
+template <typename F>
+static inline int preload_one(F* f) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f)) == cudaSuccess ? 0 : 1;
+}
+int preload_attention() {
+  return preload_one(fa_fwd_kernel) | preload_one(fa_bwd_kernel) | preload_one(fa_bwd_pre_kernel) |
+         preload_one(attn_combine_scale_kernel) | preload_one(attn_combine_finish_kernel);
+}
 }  // namespace mp
 
 using namespace mp;

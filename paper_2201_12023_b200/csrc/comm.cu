@@ -73,6 +73,26 @@ int mp_comm_destroy(void* comm) {
   return 0;
 }
 
+// Watchdog support (the deadlock half of SimError, sim.py:172-178): a hung
+// collective is released by aborting its communicator; asynchronous NCCL
+// failures (a peer died, a network error) are polled without blocking.
+int mp_comm_abort(void* comm) {
+  clear_error();
+  if (!comm) return 0;
+  MP_NCCL(ncclCommAbort(reinterpret_cast<ncclComm_t>(comm)));
+  return 0;
+}
+
+int mp_comm_async_error(void* comm, int* nccl_result) {
+  clear_error();
+  MP_CHECK_ARG(comm && nccl_result, "bad args");
+  ncclResult_t r = ncclSuccess;
+  MP_NCCL(ncclCommGetAsyncError(reinterpret_cast<ncclComm_t>(comm), &r));
+  *nccl_result = (int)r;
+  if (r != ncclSuccess && r != ncclInProgress) set_error(ncclGetErrorString(r));
+  return 0;
+}
+
 int mp_allreduce(void* comm, void* buf, int64_t count, int dtype, int op, void* stream) {
   clear_error();
   MP_CHECK_ARG(comm && buf && count >= 0 && (op == 0 || op == 1), "bad args");

@@ -161,8 +161,25 @@ ConvGeom geom(int64_t N, int64_t H, int64_t W, int64_t C, int k, int s) {
   return g;
 }
 
+
+// Force-load this file's kernels (lazy module loading would load a kernel at its
+// first launch, which blocks the host while an NCCL kernel spins on the device:
+// a deadlock the executor's watchdog could not see).  See mp_preload_kernels.
+template <typename F>
+static inline int preload_one(F* f) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f)) == cudaSuccess ? 0 : 1;
+}
+int preload_conv_impl() {
+  return preload_one(im2col_kernel<1>) | preload_one(im2col_kernel<8>) |
+         preload_one(col2im_kernel<1>) | preload_one(col2im_kernel<8>) |
+         preload_one(subsample_kernel<1>) | preload_one(subsample_kernel<8>) |
+         preload_one(reduce_mid_kernel) | preload_one(broadcast_mid_kernel);
+}
 }  // namespace
+int preload_conv() { return preload_conv_impl(); }
 }  // namespace mp
+
 
 using namespace mp;
 

@@ -997,6 +997,20 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   return 0;
 }
 
+
+// Force-load this file's kernels (lazy module loading would load a kernel at its
+// first launch, which blocks the host while an NCCL kernel spins on the device:
+// a deadlock the executor's watchdog could not see).  See mp_preload_kernels.
+template <typename F>
+static inline int preload_one(F* f) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f)) == cudaSuccess ? 0 : 1;
+}
+int preload_gemm() {
+  return preload_one(gemm_bf16_kernel<64>) | preload_one(gemm_bf16_kernel<128>) |
+         preload_one(gemm_bf16_kernel<256>) | preload_one(gemm_bf16_2sm_kernel<128>) |
+         preload_one(gemm_bf16_2sm_kernel<256>);
+}
 }  // namespace mp
 
 using namespace mp;

@@ -142,8 +142,23 @@ __global__ void moe_mask_grad_kernel(const int* __restrict__ route, const uint16
   out[i] = v;
 }
 
+
+// Force-load this file's kernels (lazy module loading would load a kernel at its
+// first launch, which blocks the host while an NCCL kernel spins on the device:
+// a deadlock the executor's watchdog could not see).  See mp_preload_kernels.
+template <typename F>
+static inline int preload_one(F* f) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f)) == cudaSuccess ? 0 : 1;
+}
+int preload_moe_impl() {
+  return preload_one(moe_route_kernel) | preload_one(moe_mask_kernel) |
+         preload_one(moe_mask_grad_kernel);
+}
 }  // namespace
+int preload_moe() { return preload_moe_impl(); }
 }  // namespace mp
+
 
 using namespace mp;
 

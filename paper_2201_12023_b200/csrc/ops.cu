@@ -482,6 +482,33 @@ __global__ void sum_parts_f32_kernel(const float4* __restrict__ parts, int64_t n
   }
 }
 
+
+// Force-load this file's kernels (lazy module loading would load a kernel at its
+// first launch, which blocks the host while an NCCL kernel spins on the device:
+// a deadlock the executor's watchdog could not see).  See mp_preload_kernels.
+template <typename F>
+static inline int preload_one(F* f) {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f)) == cudaSuccess ? 0 : 1;
+}
+int preload_ops() {
+  return preload_one(unary_bf16_kernel<ScaleF>) | preload_one(unary_bf16_kernel<GeluF>) |
+         preload_one(binary_bf16_kernel<AddF>) | preload_one(binary_bf16_kernel<GeluBwdF>) |
+         preload_one(sumsq_kernel) | preload_one(softmax_fwd_kernel) |
+         preload_one(softmax_stats_kernel) | preload_one(softmax_rescale_kernel) |
+         preload_one(softmax_apply_kernel) | preload_one(softmax_rowdot_kernel) |
+         preload_one(softmax_bwd_kernel) | preload_one(box_copy_kernel<uint32_t, false>) |
+         preload_one(box_copy_kernel<uint32_t, true>) | preload_one(box_copy_kernel<uint16_t, false>) |
+         preload_one(box_copy_kernel<uint16_t, true>) | preload_one(box_copy_kernel<uint4, false>) |
+         preload_one(box_copy_kernel<uint4, true>) | preload_one(adam_kernel) |
+         preload_one(adam4_kernel) | preload_one(cast_f32_bf16_kernel) |
+         preload_one(cast4_f32_bf16_kernel) | preload_one(cast_bf16_f32_kernel) |
+         preload_one(accum_bf16_f32_kernel) | preload_one(sum_parts_f32_kernel);
+}
+int preload_gemm();
+int preload_attention();
+int preload_conv();
+int preload_moe();
 }  // namespace mp
 
 using namespace mp;
@@ -493,6 +520,16 @@ extern "C" {
 int mp_abi_version(void) { return 1; }
 const char* mp_last_error(void) { return g_err.c_str(); }
 uint64_t mp_launch_count(void) { return g_launches.load(); }
+int mp_preload_kernels(void) {
+  clear_error();
+  const int bad = preload_ops() | preload_gemm() | preload_attention() | preload_conv() |
+                  preload_moe();
+  if (bad) {
+    set_error(std::string("kernel preload failed: ") + cudaGetErrorString(cudaGetLastError()));
+    return 1;
+  }
+  return 0;
+}
 
 int mp_gelu_fwd(const void* x, void* y, int64_t n, void* stream) {
   clear_error();

@@ -58,6 +58,9 @@ EXPORTS = {
     "mp_nccl_unique_id": ([c_vp], c_int),
     "mp_comm_init": ([c_vp, c_int, c_int, ctypes.POINTER(c_vp)], c_int),
     "mp_comm_destroy": ([c_vp], c_int),
+    "mp_comm_abort": ([c_vp], c_int),
+    "mp_preload_kernels": ([], c_int),
+    "mp_comm_async_error": ([c_vp, ctypes.POINTER(c_int)], c_int),
     "mp_allreduce": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
     "mp_allgather": ([c_vp, c_vp, c_vp, c_i64, c_int, c_vp], c_int),
     "mp_reduce_scatter": ([c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
@@ -117,6 +120,10 @@ def _check(rc: int, what: str) -> None:
     if rc != 0:
         msg = load().mp_last_error().decode(errors="replace")
         raise NativeError(f"{what} failed (rc={rc}): {msg}")
+
+
+def preload_kernels() -> None:
+    _check(load().mp_preload_kernels(), "mp_preload_kernels")
 
 
 def launch_count() -> int:
@@ -676,6 +683,17 @@ def comm_init(uid: bytes, nranks: int, rank: int) -> int:
 
 def comm_destroy(comm: int) -> None:
     _check(load().mp_comm_destroy(comm), "mp_comm_destroy")
+
+
+def comm_abort(comm: int) -> None:
+    _check(load().mp_comm_abort(comm), "mp_comm_abort")
+
+
+def comm_async_error(comm: int) -> int:
+    """ncclResult_t of the communicator's asynchronous state (0 ok, 7 in progress)."""
+    r = c_int(0)
+    _check(load().mp_comm_async_error(comm, ctypes.byref(r)), "mp_comm_async_error")
+    return int(r.value)
 
 
 def allreduce(comm: int, t: torch.Tensor, op: int = 0, stream=None) -> None:

@@ -21,9 +21,11 @@ from __future__ import annotations
 
 import math
 import os
+import json
 import time
 import zlib
 from dataclasses import dataclass, field
+from fractions import Fraction
 from typing import Callable, Optional
 
 import numpy as np
@@ -49,7 +51,18 @@ def stable_seed(*parts) -> int:
 
 class ExecError(RuntimeError):
     """Executor failure naming rank and instruction (the SimError analogue,
-    sim.py:26)."""
+    sim.py:26).  kind: "oom" (CUDA allocator, or the device_memory cap:
+    sim.py:152-160), "deadlock" (watchdog timeout: sim.py:172-178), "nccl"
+    (asynchronous communicator failure), "kernel" (a libmpexec call failed),
+    "plan" (the plan cannot be executed as given)."""
+
+    def __init__(self, msg: str, *, kind: str = "plan", rank: Optional[int] = None,
+                 stage: Optional[int] = None, instruction: Optional[str] = None):
+        super().__init__(msg)
+        self.kind = kind
+        self.rank = rank
+        self.stage = stage
+        self.instruction = instruction
 
 
 @dataclass
@@ -82,6 +95,37 @@ class ExecResult:
     # {e1, pos1|-1, e2, pos2|-1}, the decisions the parity check replays
     routes: Optional[dict] = None
 
+    def trace_json(self) -> str:
+        """The reference's sim.json document (SimResult.trace_json, sim.py:46-57)
+        with measured seconds: makespan as an exact [num, den] of whole
+        nanoseconds, utilization per stage, peak bytes per device, every
+        instruction's event.  Extra key: "measured": true."""
+        ns = Fraction(round(self.makespan * 1e9), 10 ** 9)
+        doc = {
+            "makespan": [ns.numerator, ns.denominator],
+            "makespan_seconds": float(self.makespan),
+            "utilization": {str(k): float(v) for k, v in sorted(self.utilization.items())},
+            "peak_bytes": {str(k): int(v) for k, v in sorted(self.peak_bytes.items())},
+            "events": [{"stage": e.stage, "op": e.op, "label": e.label,
+                        "start": float(e.start), "end": float(e.end)} for e in self.events],
+            "measured": True,
+        }
+        return json.dumps(doc, sort_keys=True, indent=2)
+
+    def gantt_rows(self, program) -> dict[str, list[list]]:
+        """Per-device rows of [start, end, label] of the busy instructions
+        (compute / send / all_gather) of the device's stage (sim.py:59-71)."""
+        by_stage: dict[int, list[ExecEvent]] = {}
+        for e in self.events:
+            if e.op in BUSY_OPS:
+                by_stage.setdefault(e.stage, []).append(e)
+        rows: dict[str, list[list]] = {}
+        for sp in program.stages:
+            seq = [[float(e.start), float(e.end), e.label] for e in by_stage.get(sp.stage, [])]
+            for dev in sp.device_ids:
+                rows[str(dev)] = seq
+        return rows
+
 
 @dataclass
 class AdamConfig:
@@ -91,6 +135,11 @@ class AdamConfig:
     eps: float = 1e-8
     weight_decay: float = 0.0
 
+
+BUSY_OPS = ("compute", "send", "all_gather")      # sim.py:23
+# watchdog: a step whose device work has not finished after this many seconds
+# is a deadlock (ExecError naming the first unfinished instruction)
+STEP_TIMEOUT_S = float(os.environ.get("MPEXEC_STEP_TIMEOUT_S", "600"))
 
 GATHER_ANY_DIM = os.environ.get("MPEXEC_GATHER_ANY_DIM", "1") != "0"
 FUSE_BMM_EPI = os.environ.get("MPEXEC_FUSE_BMM_EPILOGUE", "1") == "1"
@@ -1236,7 +1285,7 @@ class StageRunner:
                     out = self._run_elementwise(mb, op)
             except native.NativeError as e:
                 raise ExecError(f"rank {self.me} stage {self.st.index} {phase}{mb} node "
-                                f"{op.nid} ({op.op}): {e}") from None
+                                f"{op.nid} ({op.op}): {e}", kind="kernel") from None
             if out is not None:
                 vals[op.nid] = out
 
@@ -1338,8 +1387,14 @@ class StageRunner:
             sends.append((view if view is not None else native.pack_box(v, lo, ext), t.dst_device))
         if sends:
             self.send_stream.wait_stream(torch.cuda.current_stream())
+            rec = getattr(self, "_recording", False)
+            ea = torch.cuda.Event(enable_timing=rec)
+            eb = torch.cuda.Event(enable_timing=rec)
+            ea.record(self.send_stream)
             self.comm.p2p(sends, [], self.comm.boundary_group(bd, self.plan),
                           stream=self.send_stream)
+            eb.record(self.send_stream)
+            self._send_ev = (ea, eb)
             for buf, _ in sends:
                 buf.record_stream(self.send_stream)
             if self.use_graphs:
@@ -1461,42 +1516,76 @@ class StageRunner:
         return self.gradbuf[off:off + math.prod(ld)].view(ld)
 
     # ------------------------------------------------------------------ step
+    def _dispatch(self, ins: Instr, update: bool) -> None:
+        if ins.op == "compute":
+            self.compute(ins.phase, ins.microbatch)
+        elif ins.op == "recv":
+            self.recv(ins)
+        elif ins.op == "send":
+            self.send(ins)
+        elif ins.op == "all_gather":
+            self.all_gather(ins)
+        elif ins.op == "free":
+            self.free(ins)
+        elif ins.op == "sync":
+            if self.sends_pending:
+                torch.cuda.current_stream().wait_stream(self.send_stream)
+                self.sends_pending = False
+            if update:
+                self.optimizer_step()
+
     def run_step(self, *, record: bool = False, update: bool = True):
-        """Run the stage's instruction list once; returns measured events."""
+        """Enqueue the stage's instruction list once.  Returns (t0, t1, events,
+        markers): step start / end events, with record=True a timing event pair
+        per instruction (sends timed on the send stream), and one completion
+        marker per instruction (the watchdog's progress record).  A failing
+        instruction raises ExecError naming rank, stage and instruction."""
         self.zero_grads()
         self.loss_acc.zero_()
         events = []
+        markers = []
         stream = torch.cuda.current_stream()
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
+        self._send_ev = None
         for ins in self.sprog.instructions:
-            if record and ins.op in ("compute", "send", "recv", "all_gather"):
+            e0 = None
+            if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            if ins.op == "compute":
-                self.compute(ins.phase, ins.microbatch)
-            elif ins.op == "recv":
-                self.recv(ins)
-            elif ins.op == "send":
-                self.send(ins)
-            elif ins.op == "all_gather":
-                self.all_gather(ins)
-            elif ins.op == "free":
-                self.free(ins)
-            elif ins.op == "sync":
-                if self.sends_pending:
-                    torch.cuda.current_stream().wait_stream(self.send_stream)
-                    self.sends_pending = False
-                if update:
-                    self.optimizer_step()
-            if record and ins.op in ("compute", "send", "recv", "all_gather"):
-                e1 = torch.cuda.Event(enable_timing=True)
-                e1.record(stream)
+            self._recording = record
+            try:
+                self._dispatch(ins, update)
+            except torch.cuda.OutOfMemoryError as e:
+                raise ExecError(
+                    f"out of memory on device {self.me} (stage {self.st.index}) at {ins.op} "
+                    f"{ins.buffer or _label(ins)}: {torch.cuda.memory_allocated(self.dev)} bytes "
+                    f"allocated ({str(e).splitlines()[0]})", kind="oom", rank=self.me,
+                    stage=self.st.index, instruction=_label(ins)) from None
+            except ExecError as e:
+                if e.rank is None:
+                    e.rank, e.stage, e.instruction = self.me, self.st.index, _label(ins)
+                raise
+            except native.NativeError as e:
+                raise ExecError(f"rank {self.me} stage {self.st.index} at {ins.op} "
+                                f"{_label(ins)}: {e}", kind="kernel", rank=self.me,
+                                stage=self.st.index, instruction=_label(ins)) from None
+            if ins.op == "send" and self._send_ev is not None:
+                a, b = self._send_ev
+                self._send_ev = None
+                if record:
+                    events.append((ins, a, b))
+                markers.append((ins, b))
+                continue
+            e1 = torch.cuda.Event(enable_timing=record)
+            e1.record(stream)
+            if record:
                 events.append((ins, e0, e1))
+            markers.append((ins, e1))
         self.join_dw()
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(stream)
-        return t0, t1, events
+        return t0, t1, events, markers
 
 
 def _label(ins: Instr) -> str:
@@ -1523,6 +1612,7 @@ class Executor:
         if not torch.cuda.is_available():
             raise ExecError("the executor needs a CUDA device; there is no CPU execution path")
         native.load()
+        native.preload_kernels()
         self.plan = plan if isinstance(plan, ExecPlan) else load_plan(plan)
         self.program = program or build_program(self.plan, schedule)
         self.rank = dist.get_rank() if dist.is_initialized() else 0
@@ -1530,9 +1620,15 @@ class Executor:
         if self.world != self.plan.num_devices:
             raise ExecError(f"plan needs {self.plan.num_devices} devices, running on {self.world}")
         self.comm = Comm(self.plan, self.program, self.rank, self.world)
-        self.runner = StageRunner(self.plan, self.program, self.rank, self.comm, seed=seed,
-                                  params=params, inputs=inputs, adam=adam,
-                                  host_inputs=host_inputs)
+        try:
+            self.runner = StageRunner(self.plan, self.program, self.rank, self.comm, seed=seed,
+                                      params=params, inputs=inputs, adam=adam,
+                                      host_inputs=host_inputs)
+        except torch.cuda.OutOfMemoryError as e:
+            st = self.plan.stage_of_device(self.rank).index
+            raise ExecError(f"out of memory on device {self.rank} (stage {st}) at init "
+                            f"(parameters and optimizer state): {str(e).splitlines()[0]}",
+                            kind="oom", rank=self.rank, stage=st, instruction="init") from None
         self.step_times: list[float] = []
         self.last_events: list = []
 
@@ -1540,16 +1636,57 @@ class Executor:
         if self.world > 1:
             dist.barrier(group=self.comm.world_group)
 
-    def step(self, *, record: bool = False, update: bool = True) -> float:
-        """One step; returns this rank's device time (seconds)."""
-        t0, t1, evs = self.runner.run_step(record=record, update=update)
-        torch.cuda.synchronize()
+    def step(self, *, record: bool = False, update: bool = True,
+             timeout: Optional[float] = None) -> float:
+        """One step; returns this rank's device time (seconds).  The host waits
+        for the device under a watchdog: past `timeout` seconds (default
+        MPEXEC_STEP_TIMEOUT_S) the communicators are aborted and ExecError
+        (kind "deadlock") names the first instruction that has not completed;
+        an asynchronous NCCL failure raises ExecError (kind "nccl")."""
+        t0, t1, evs, markers = self.runner.run_step(record=record, update=update)
+        self._wait(t1, markers, STEP_TIMEOUT_S if timeout is None else timeout)
         dt = t0.elapsed_time(t1) * 1e-3
         self.step_times.append(dt)
         if record:
             self.last_events = [(ins, t0.elapsed_time(a) * 1e-3, t0.elapsed_time(b) * 1e-3)
                                 for ins, a, b in evs]
         return dt
+
+    def _wait(self, done: torch.cuda.Event, markers, timeout: float) -> None:
+        if done.query():
+            return
+        start = time.monotonic()
+        nap, last_poll = 5e-5, start
+        while not done.query():
+            time.sleep(nap)
+            nap = min(nap * 2, 2e-3)
+            now = time.monotonic()
+            if self.comm.enabled and now - last_poll > 1.0:
+                last_poll = now
+                bad = self.comm.async_errors()
+                if bad:
+                    ins = self._first_pending(markers)
+                    self.comm.abort()
+                    raise ExecError(f"NCCL failure on rank {self.rank} (stage "
+                                    f"{self.runner.st.index}) at {_describe(ins)}: "
+                                    + "; ".join(bad), kind="nccl", rank=self.rank,
+                                    stage=self.runner.st.index,
+                                    instruction=_label(ins) if ins else None)
+            if now - start > timeout:
+                ins = self._first_pending(markers)
+                self.comm.abort()
+                raise ExecError(f"deadlock: rank {self.rank} stage {self.runner.st.index} "
+                                f"waiting on {_describe(ins)} after {timeout:.0f} s",
+                                kind="deadlock", rank=self.rank, stage=self.runner.st.index,
+                                instruction=_label(ins) if ins else None)
+        done.synchronize()
+
+    @staticmethod
+    def _first_pending(markers):
+        for ins, ev in markers:
+            if not ev.query():
+                return ins
+        return None
 
     def loss(self) -> float:
         loss = self.runner.loss_acc.clone()
@@ -1565,12 +1702,31 @@ class Executor:
         return float(t.item())
 
     def result(self, grads=None, outputs=None, launches: int = 0) -> ExecResult:
+        """SimResult-shaped summary of the last step, gathered over all ranks
+        (sim.py:39-44): utilization of every stage (its first device's busy
+        compute / send / all_gather time over the makespan), the allocator
+        peak of every device, and every stage's instruction events (measured
+        from the step start, which a barrier aligns across ranks), sorted like
+        the simulator's (start, stage, end, label)."""
         makespan = self.max_over_ranks(self.step_times[-1]) if self.step_times else 0.0
         evs = self.last_events
-        events = [ExecEvent(ins.stage, ins.op, _label(ins), s, e) for ins, s, e in evs]
-        busy = sum(e - s for ins, s, e in evs if ins.op in ("compute", "send", "all_gather"))
-        util = {self.runner.st.index: busy / makespan if makespan > 0 else 0.0}
-        peak = {self.rank: int(torch.cuda.max_memory_allocated())}
+        st = self.runner.st
+        mine = {"rank": self.rank, "stage": st.index,
+                "leader": self.rank == min(st.mesh.device_ids),
+                "events": [(ins.stage, ins.op, _label(ins), s, e) for ins, s, e in evs],
+                "busy": sum(e - s for ins, s, e in evs if ins.op in BUSY_OPS),
+                "peak": int(torch.cuda.max_memory_allocated())}
+        parts = [mine]
+        if self.world > 1:
+            parts = [None] * self.world
+            dist.all_gather_object(parts, mine, group=self.comm.world_group)
+        util, peak, events = {}, {}, []
+        for p in parts:
+            peak[p["rank"]] = p["peak"]
+            if p["leader"]:
+                util[p["stage"]] = p["busy"] / makespan if makespan > 0 else 0.0
+                events += [ExecEvent(*e) for e in p["events"]]
+        events.sort(key=lambda e: (e.start, e.stage, e.end, e.label))
         r = self.runner
         return ExecResult(makespan=makespan, utilization=util, peak_bytes=peak, events=events,
                           modeled_makespan=float(modeled_makespan(self.program, self.plan)),
@@ -1585,11 +1741,18 @@ class Executor:
                                  "token_split_dw": len(r.tok_dw)})
 
 
+def _describe(ins: Optional[Instr]) -> str:
+    if ins is None:
+        return "the step's end"
+    return f"{ins.op} {ins.tag or ins.buffer or _label(ins)}"
+
+
 def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, steps: int = 1,
             params: Optional[dict[int, np.ndarray]] = None,
             inputs: Optional[Callable[[int, int], np.ndarray]] = None,
             seed: int = 0, adam: Optional[AdamConfig] = None, record: bool = True,
-            collect: bool = False, update: bool = True) -> ExecResult:
+            collect: bool = False, update: bool = True, device_memory: Optional[int] = None,
+            enforce_memory: bool = True, timeout: Optional[float] = None) -> ExecResult:
     """Run `steps` training steps of a reference plan on this process's GPU.
 
     The drop-in for `simulate(emit_instructions(plan, schedule), ...)`: call on
@@ -1597,7 +1760,17 @@ def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, s
     `inputs` (global fp32 arrays, identical on every rank) make runs reproducible
     against the CPU oracle; by default weights and inputs are synthetic (seeded).
     With collect=True the result carries the global parameter gradients of the
-    last step (before its update) and the forward outputs."""
+    last step (before its update) and the forward outputs.
+
+    Errors (the simulator's contract, sim.py:152-178): device_memory (bytes;
+    default: none beyond the GPU's own) caps this process's CUDA allocator when
+    enforce_memory is set, and any allocation past it raises ExecError kind
+    "oom" naming the device, stage and instruction; a step that does not finish
+    within `timeout` seconds raises kind "deadlock" naming the instruction the
+    stage is blocked on."""
+    if device_memory is not None and enforce_memory and torch.cuda.is_available():
+        total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
+        torch.cuda.set_per_process_memory_fraction(min(1.0, device_memory / total))
     ex = Executor(plan, program, schedule=schedule, params=params, inputs=inputs, seed=seed,
                   adam=adam)
     ex.runner.keep_outputs = collect
@@ -1607,7 +1780,8 @@ def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, s
         last = step == steps - 1
         ex.barrier()
         torch.cuda.synchronize()
-        ex.step(record=record and last, update=update and not (collect and last))
+        ex.step(record=record and last, update=update and not (collect and last),
+                timeout=timeout)
         if last and collect:
             ex.runner.reduce_grads()
             grads = _collect_grads(ex.runner, ex.comm, ex.world)
