@@ -233,6 +233,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--plan", default=None)
+    ap.add_argument("--nvtx-step", action="store_true",
+                    help="after the warm-up, run ONE step inside an NVTX range 'step' and exit "
+                         "(for `ncu --nvtx --nvtx-include step/`: a steady-state launch list "
+                         "covering a whole step, Adam included); prints nothing else")
     ap.add_argument("--workload", default="gpt", choices=sorted(WORKLOADS),
                     help="default plan plans/<gpt13b|moe24b>_n<N>/plan.json")
     args = ap.parse_args()
@@ -262,6 +266,16 @@ def main():
 
     for _ in range(args.warmup):
         ex.step()
+    if args.nvtx_step:
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("step")
+        ex.runner.run_step(record=False, update=True)
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
     # ---- timed region: device-resident inputs
     native.gemm_timer = []
     clocks = ClockSampler(local)
