@@ -122,6 +122,32 @@ def cpu_baseline_sample(threads: int):
     return flops / dt / 1e12, dt, flops
 
 
+def orchestration_port_sample(plan_path, reps: int = 3):
+    """The reference's own CPU path for one step of this plan, as ported here:
+    emit_instructions (schedule.build_program, instruction lists identical to the
+    reference's) + simulate (schedule.modeled_makespan, the simulator's timing
+    rules in exact rationals; makespans equal to the reference's).  One core
+    (the reference is single-threaded).  Returns a dict of per-step ms."""
+    sys.path.insert(0, str(ROOT))
+    from paper_2201_12023_b200.plan import load_plan
+    from paper_2201_12023_b200.schedule import build_program, modeled_makespan
+    plan = load_plan(plan_path)
+    emit, sim = [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        prog = build_program(plan, "1f1b")
+        t1 = time.perf_counter()
+        modeled_makespan(prog, plan)
+        t2 = time.perf_counter()
+        emit.append(t1 - t0)
+        sim.append(t2 - t1)
+    n = sum(len(sp.instructions) for sp in prog.stages)
+    return {"emit_instructions_ms": statistics.median(emit) * 1e3,
+            "simulate_ms": statistics.median(sim) * 1e3, "instructions": n, "cores": 1,
+            "basis": "restated reference.emit_instructions + simulate (programs and "
+                     "makespans pinned equal to the reference's, tests/golden)"}
+
+
 def run_reference(args):
     """--impl reference: the CPU implementation of the path (oracle port, numpy,
     all host threads) on a bounded sample of the same workload; rank 0 only."""
@@ -151,6 +177,10 @@ def run_reference(args):
                                    "extrapolated to the full step at constant rate" % dt},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        out["cpu_baseline"]["orchestration_port"] = orchestration_port_sample(plan_path)
+    except Exception as e:      # noqa: BLE001
+        out["cpu_baseline"]["orchestration_port"] = {"error": str(e)[:200]}
     print(json.dumps(out), flush=True)
     return 0
 
@@ -222,6 +252,34 @@ def _config(n, doc, plan_rel):
         "schedule": "1f1b",
         "l2": "no flush needed: per-step working set (2.4 GB weights + activations) >> 126 MB L2",
     }
+
+
+def _xmesh_leg(rank, world):
+    """Config-5 sweep (scripts/xmesh_sweep.py) after the measured steps; the full
+    row list goes to gpurun_out/xmesh_bench.jsonl, the line gets the best bus GB/s
+    per (src, dst, optimize) and size.  Never fails the bench."""
+    import torch
+    t0 = time.perf_counter()
+    try:
+        sys.path.insert(0, str(ROOT / "scripts"))
+        import xmesh_sweep
+        torch.cuda.synchronize()
+        path = ROOT / "gpurun_out" / "xmesh_bench.jsonl"
+        out = None
+        if rank == 0:
+            path.parent.mkdir(exist_ok=True)
+            out = open(path, "w")
+        rows = xmesh_sweep.sweep(rank, world, xmesh_sweep.SIZES_MIB, out, log=None, iters=5)
+        if rank != 0:
+            return None
+        return {"bus_gbs_best": xmesh_sweep.summarize(rows), "cases": len(rows),
+                "peak_gbs": 900.0, "sizes_mib": xmesh_sweep.SIZES_MIB,
+                "seconds": round(time.perf_counter() - t0, 1),
+                "basis": "max over devices of (egress or ingress bytes) / time (max over ranks, "
+                         "CUDA events); plans from xmesh.cross_mesh_plan (reshard.py:111-157)"}
+    except Exception as e:      # noqa: BLE001 - a sweep failure must not void the bench line
+        return {"error": f"{type(e).__name__}: {e}"[:300],
+                "seconds": round(time.perf_counter() - t0, 1)}
 
 
 def main():
@@ -352,6 +410,12 @@ def main():
         ex.runner.input_mode = "resident"
 
     loss = ex.loss()
+    # ---- config 5 (BASELINE configs[4]): the cross-mesh resharding sweep between
+    # (1,1)/(1,2)/(1,4) submeshes, 1 MiB .. 1 GiB, optimize on / off.  Every pair needs
+    # src + dst GPUs, so the full set (incl. (1,4) -> (1,4)) runs on the 8-GPU step.
+    xmesh = None
+    if world >= 8 or os.environ.get("MPEXEC_BENCH_XMESH") == "1":
+        xmesh = _xmesh_leg(rank, world)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -391,12 +455,15 @@ def main():
     }
     if e2e:
         out["e2e"] = e2e
+    if xmesh is not None:
+        out["xmesh"] = xmesh
     if args.gpus == 1 and not args.no_cpu_baseline:
         v, dt, fl = cpu_baseline_sample(len(os.sched_getaffinity(0)))
         out["cpu_baseline"] = {
             "value": v, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "port",
             "sample": "oracle/dense.py numpy float32: 1 GPT-1.3B block x 1 microbatch "
-                      "(8 x 1024 tokens) fwd+bwd, %.2f s (%.3g FLOP)" % (dt, fl)}
+                      "(8 x 1024 tokens) fwd+bwd, %.2f s (%.3g FLOP)" % (dt, fl),
+            "orchestration_port": orchestration_port_sample(plan_path)}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -230,6 +230,7 @@ class StageRunner:
         self.cap_aux: dict = {}
         self.static: dict = {}
         self.slot_send_ev: dict[int, torch.cuda.Event] = {}
+        self.cap_out: dict = {}
 
         self.input_mode = "host" if host_inputs else ("fn" if inputs is not None else "resident")
         self._resident_inputs: dict = {}
@@ -1249,18 +1250,23 @@ class StageRunner:
             before = set(vals)
             g = torch.cuda.CUDAGraph()
             self.join_dw()
+            had_out = mb in self.outputs
             with torch.cuda.graph(g):
                 self._compute_eager(phase, mb, skip_inputs=True)
                 self.join_dw()
             self.graphs[key] = g
             self.cap_vals[key] = {n: v for n, v in vals.items() if n not in before}
             self.cap_aux[key] = dict(self.aux.get(mb, {}))
+            if self.keep_outputs and not had_out and mb in self.outputs:
+                self.cap_out[key] = self.outputs[mb]      # the slot's static output buffer
             g.replay()
-            return
-        vals.update(self.cap_vals[key])
-        if self.cap_aux[key]:
-            self.aux.setdefault(mb, {}).update(self.cap_aux[key])
-        g.replay()
+        else:
+            vals.update(self.cap_vals[key])
+            if self.cap_aux[key]:
+                self.aux.setdefault(mb, {}).update(self.cap_aux[key])
+            g.replay()
+        if key in self.cap_out:            # a replay rewrites the buffer: keep a copy
+            self.outputs[mb] = self.cap_out[key].clone()
 
     def _compute_eager(self, phase: str, mb: int, skip_inputs: bool = False):
         vals = self.vals.setdefault(mb, {})

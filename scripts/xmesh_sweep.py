@@ -16,7 +16,10 @@ and bus GB/s = max over devices of (egress or ingress bytes) / time, against
 900 GB/s/dir nominal (770 measured peer copy).
 
   python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
-      scripts/xmesh_sweep.py [--sizes-mib 1,16,256,1024] [--out gpurun_out/xmesh.jsonl]
+      scripts/xmesh_sweep.py [--sizes-mib 1,2,4,...,1024] [--out gpurun_out/xmesh.jsonl]
+
+bench.py runs the same sweep (every size, every pair that fits) after its 8-GPU
+measurement and adds the per-pair best bus GB/s to its JSON line (`xmesh`).
 """
 import argparse
 import itertools
@@ -51,6 +54,8 @@ def specs_2d(mesh: Mesh, dims):
 
 
 def run_case(rank, dims, sspec, smesh, dspec, dmesh, optimize, groups, iters=5):
+    """-> (seconds per reshard, max over ranks; inter-mesh bytes; algorithmic bytes;
+    busiest device's egress-or-ingress bytes)."""
     xp = cross_mesh_plan(dims, 2, sspec, smesh, dspec, dmesh, optimize)
     dev = torch.device("cuda", torch.cuda.current_device())
     src_local = dst_local = None
@@ -145,23 +150,15 @@ def run_case(rank, dims, sspec, smesh, dspec, dmesh, optimize, groups, iters=5):
     return float(t.item()), xp.inter_mesh_bytes, algo, peak_dev
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--sizes-mib", default="1,16,256,1024")
-    ap.add_argument("--out", default=str(ROOT / "gpurun_out/xmesh_sweep.jsonl"))
-    args = ap.parse_args()
-    world = int(os.environ["WORLD_SIZE"])
-    rank = int(os.environ["RANK"])
-    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
-    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
-    native.load()
+SIZES_MIB = [1 << i for i in range(11)]            # 1 MiB .. 1 GiB
+
+
+def make_groups(world):
     shapes = [(1, 1), (1, 2), (1, 4)]
     pairs = [(s, d) for s in shapes for d in shapes if s[1] + d[1] <= world]
     groups = {"world": dist.new_group(list(range(world))), "pair": dist.new_group(list(range(world)))}
     for s, d in pairs:
         dm = Mesh(1, d[1], tuple(range(s[1], s[1] + d[1])))
-        for sz in range(2, d[1] + 1):
-            pass
         # every gather group a replica spec can form inside dst
         for k in (2, 4):
             if k <= d[1]:
@@ -169,12 +166,19 @@ def main():
                     devs = tuple(range(s[1] + start, s[1] + start + k))
                     if ("gather", devs) not in groups:
                         groups[("gather", devs)] = dist.new_group(list(devs))
-        # all of dst too
         devs = tuple(dm.device_ids)
         if len(devs) > 1 and ("gather", devs) not in groups:
             groups[("gather", devs)] = dist.new_group(list(devs))
-    out = open(args.out, "a") if rank == 0 else None
-    for mib in [int(x) for x in args.sizes_mib.split(",")]:
+    return pairs, groups
+
+
+def sweep(rank, world, sizes_mib, out=None, log=print, iters=5):
+    """Every (src, dst) pair of {(1,1),(1,2),(1,4)} that fits on `world` GPUs
+    (src on the first devices, dst on the next), every spec pair, both optimize
+    settings, every size.  Returns the rows (rank 0; None elsewhere)."""
+    pairs, groups = make_groups(world)
+    rows_out = [] if rank == 0 else None
+    for mib in sizes_mib:
         rows = mib * 1024 * 1024 // (8192 * 2)
         dims = (rows, 8192)
         for s, d in pairs:
@@ -185,24 +189,58 @@ def main():
                     res = {}
                     for opt in (True, False):
                         try:
-                            t, inter, algo, peak = run_case(rank, dims, ss, sm, ds, dm, opt, groups)
-                        except KeyError as e:
-                            t, inter, algo, peak = float("nan"), 0, 0, 1
-                        res[opt] = (t, inter, algo, peak)
-                    if rank == 0:
-                        for opt in (True, False):
-                            t, inter, algo, peak = res[opt]
-                            row = {"mib": mib, "src": list(s), "dst": list(d), "src_spec": format_spec(ss),
-                                   "dst_spec": format_spec(ds), "optimize": opt, "time_s": t,
-                                   "inter_mesh_bytes": inter, "algorithmic_bytes": algo,
-                                   "bus_gbs": peak / t / 1e9 if t == t and t > 0 else None,
-                                   "speedup_vs_naive": res[False][0] / t if opt else None}
+                            res[opt] = run_case(rank, dims, ss, sm, ds, dm, opt, groups, iters)
+                        except KeyError:
+                            res[opt] = (float("nan"), 0, 0, 1)
+                    if rank != 0:
+                        continue
+                    for opt in (True, False):
+                        t, inter, algo, peak = res[opt]
+                        row = {"mib": mib, "src": list(s), "dst": list(d),
+                               "src_spec": format_spec(ss), "dst_spec": format_spec(ds),
+                               "optimize": opt, "time_s": t, "inter_mesh_bytes": inter,
+                               "algorithmic_bytes": algo,
+                               "bus_gbs": peak / t / 1e9 if t == t and t > 0 else None,
+                               "speedup_vs_naive": res[False][0] / t if opt else None}
+                        rows_out.append(row)
+                        if out is not None:
                             out.write(json.dumps(row) + "\n")
                             out.flush()
-                            if opt:
-                                print(f"{mib:5d} MiB {s}->{d} {format_spec(ss):>6}->{format_spec(ds):<6} "
-                                      f"opt {t*1e3:8.3f} ms  naive {res[False][0]*1e3:8.3f} ms  "
-                                      f"x{res[False][0]/t:4.2f}  bus {row['bus_gbs']:.0f} GB/s", flush=True)
+                        if opt and log is not None:
+                            log(f"{mib:5d} MiB {s}->{d} {format_spec(ss):>6}->{format_spec(ds):<6} "
+                                f"opt {t*1e3:8.3f} ms  naive {res[False][0]*1e3:8.3f} ms  "
+                                f"x{res[False][0]/t:4.2f}  bus {row['bus_gbs']:.0f} GB/s")
+    return rows_out
+
+
+def summarize(rows):
+    """Per (src, dst, optimize): best bus GB/s over spec pairs at each size."""
+    best = {}
+    for r in rows:
+        if r["bus_gbs"] is None:
+            continue
+        k = (f"{r['src'][1]}->{r['dst'][1]}", "opt" if r["optimize"] else "naive")
+        cur = best.setdefault(k, {})
+        cur[r["mib"]] = max(cur.get(r["mib"], 0.0), round(r["bus_gbs"], 1))
+    return {f"(1,{k[0].split('->')[0]})->(1,{k[0].split('->')[1]}) {k[1]}": v
+            for k, v in sorted(best.items())}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes-mib", default=",".join(str(x) for x in SIZES_MIB))
+    ap.add_argument("--out", default=str(ROOT / "gpurun_out/xmesh_sweep.jsonl"))
+    args = ap.parse_args()
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+    native.load()
+    out = open(args.out, "a") if rank == 0 else None
+    rows = sweep(rank, world, [int(x) for x in args.sizes_mib.split(",")], out,
+                 log=lambda m: print(m, flush=True))
+    if rank == 0:
+        print(json.dumps({"summary_best_bus_gbs": summarize(rows)}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

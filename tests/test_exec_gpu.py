@@ -128,3 +128,13 @@ def test_zero_rewrite_matches_allreduce_training():
     assert a[2] < a[0], a                      # it trains
     for x, y in zip(a, b):
         assert abs(x - y) <= 1e-3 * abs(y), (a, b)
+
+
+@pytest.mark.parametrize("plan", ["plans/mlp_n1/plan.json", "plans/tiny_gpt_n1/plan.json"])
+def test_cuda_graph_mode_parity(plan, monkeypatch):
+    """MPEXEC_CUDA_GRAPHS=1: one capture per (phase, slot), replays for the other
+    microbatches; loss, gradients and the collected outputs match the oracle."""
+    monkeypatch.setenv("MPEXEC_CUDA_GRAPHS", "1")
+    errs = run_plan(ROOT / plan, "1f1b")
+    print(json.dumps(errs))
+    assert errs["ok"], errs
