@@ -1,7 +1,8 @@
-"""Run the reference planner CLI (`meshplan plan ...`) with its intra-op ILP
-solver swapped for the native one (paper_2201_12023_b200/ilp.py).
-Plans are byte-identical to the pure-Python planner's (tests/test_ilp_native.py);
-only the solve time changes.
+"""Run the reference planner CLI (`meshplan plan ...`) with its intra-op strategy
+table (intra.py:196-238) and ILP solver (intra.py:323-401) swapped for the native
+ones (paper_2201_12023_b200/ilp.py).  Plans are byte-identical to the
+pure-Python planner's (tests/test_ilp_native.py); only the planning time changes:
+GPT-1.3B on (1,8) at L=4 (plans/gpt13b_n8_L4) 660 s pure Python -> 7.5 s.
 
   python scripts/plan_native.py --reference-src /root/reference/pkg/src -- \
       plan --builder transformer:... --cluster plans/clusters/b200_1x8.json --out DIR

@@ -136,3 +136,66 @@ def test_native_matches_reference_on_real_stage_ilps(meshplan_ref):
             assert got.certified == ref.certified
             n_checked += 1
     assert n_checked >= 4
+
+
+@pytest.mark.reference
+def test_native_table_equals_reference_table(meshplan_ref):
+    """ilp.build_ilp (int64 edge assembly, memoised algorithms / costs) builds the
+    reference's strategy table entry for entry: same algorithms, node costs and
+    exact edge-matrix Fractions on every view of a 1-block GPT on (1,2) and (1,4)."""
+    from meshplan.costs import CostModel
+    from meshplan.graph import build_transformer_blocks
+    from meshplan.intra import build_ilp, extract_stage, merge_trivial, solve_ilp
+    from meshplan.mesh import ClusterMesh, SubmeshShape, logical_views
+    from meshplan.sharding import SpecError
+    from paper_2201_12023_b200 import ilp
+    g = build_transformer_blocks(1, 2, 32, 64, 4, elem_bytes=2, backward=True)
+    checked = 0
+    for m in (2, 4):
+        cl = ClusterMesh(1, m, 900 * 10**9, 900 * 10**9, Fraction(1, 100000), 14 * 10**14,
+                         18 * 10**10)
+        cm = CostModel(cl)
+        merged = merge_trivial(extract_stage(g, range(len(g))))
+        for view in logical_views(SubmeshShape(1, m), cl):
+            try:
+                ref = build_ilp(merged, view, cm)
+            except SpecError:
+                continue
+            got = ilp.build_ilp(merged, view, cm)
+            assert got.algorithms == ref.algorithms and got.c == ref.c and got.d == ref.d
+            assert [(u, v) for u, v, _ in got.edges] == [(u, v) for u, v, _ in ref.edges]
+            for (_, _, gm), (_, _, rm) in zip(got.edges, ref.edges):
+                assert [list(r) for r in gm] == [list(r) for r in rm]
+            a, b = ilp.solve_ilp(got), solve_ilp(ref)
+            assert (a.choice, a.objective, a.certified) == (b.choice, b.objective, b.certified)
+            assert got.evaluate(a.choice) == ref.evaluate(b.choice)
+            checked += 1
+    assert checked >= 4
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("builder,cluster,b,layers", [
+    ("mlp:layers=2,batch=64,hidden=1024,backward=1", "b200_1x4.json", 4, 2),
+    ("transformer:blocks=1,batch=2,seq=32,hidden=64,heads=4,elem_bytes=2,backward=1",
+     "b200_1x4.json", 3, 1),
+])
+def test_patched_planner_writes_identical_plans(meshplan_ref, tmp_path, builder, cluster, b,
+                                                layers):
+    """The whole reference planner with the native table + solver swapped in
+    writes the same plan.json bytes as the untouched planner."""
+    import subprocess
+    import sys
+    root = Path(__file__).resolve().parent.parent
+    outs = {}
+    for mode in ("native", "python"):
+        cmd = [sys.executable, str(root / "scripts/plan_native.py")]
+        if mode == "python":
+            cmd.append("--python-solver")
+        cmd += ["--", "plan", "--builder", builder, "--cluster",
+                str(root / "plans/clusters" / cluster), "--b", str(b), "--layers", str(layers),
+                "--epsilon", "0", "--schedule", "1f1b", "--out", str(tmp_path / mode)]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+                           env={**__import__("os").environ, "PYTHONPATH": str(root)})
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[mode] = (tmp_path / mode / "plan.json").read_bytes()
+    assert outs["native"] == outs["python"]
