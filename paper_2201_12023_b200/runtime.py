@@ -205,6 +205,9 @@ class StageRunner:
                           else None)
         self.dw_pending = False
         self.g_fresh: set[int] = set()
+        # MPEXEC_OP_TIMING=1: CUDA events around every op and relayout (analysis only)
+        self.op_timer = [] if os.environ.get("MPEXEC_OP_TIMING") == "1" else None
+        self.relayout_timer: list = []
         self._compile()
         self._init_params(params)
         self.step_count = 0
@@ -706,6 +709,18 @@ class StageRunner:
         have, req = canonical(have, self.mesh), canonical(req, self.mesh)
         if have == req:
             return v
+        if self.op_timer is None:
+            return self._coerce_impl(v, dims, have, req)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = self._coerce_impl(v, dims, have, req)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        kind, _ = self._relayout_plan(tuple(dims), have, req)
+        self.relayout_timer.append((kind, math.prod(dims) * v.element_size(), e0, e1))
+        return out
+
+    def _coerce_impl(self, v, dims, have: Spec, req: Spec) -> torch.Tensor:
         kind, info = self._relayout_plan(tuple(dims), have, req)
         if kind == "local":
             return self._narrow(v, info)
@@ -1270,7 +1285,12 @@ class StageRunner:
 
     def _compute_eager(self, phase: str, mb: int, skip_inputs: bool = False):
         vals = self.vals.setdefault(mb, {})
+        timer = self.op_timer
         for op in (self.fwd_ops if phase == "fwd" else self.bwd_ops):
+            if timer is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                r0 = len(self.relayout_timer)
             try:
                 if op.op == "input":
                     if skip_inputs:
@@ -1294,6 +1314,10 @@ class StageRunner:
                                 f"{op.nid} ({op.op}): {e}", kind="kernel") from None
             if out is not None:
                 vals[op.nid] = out
+            if timer is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                timer.append((phase, op.op, e0, e1, self.relayout_timer[r0:]))
 
     def recv(self, ins: Instr):
         bd = ins.boundary

@@ -27,6 +27,7 @@ def census(plan_path, device):
     r.bound = runtime.bind(plan.graph)
     r.cons = plan.graph.consumers()
     r._moves_cache, r._plans = {}, {}
+    r.op_timer, r.relayout_timer = None, []
     r._compile()
     rows = Counter()
     nbytes = Counter()
