@@ -25,6 +25,8 @@ from dataclasses import dataclass, field
 import torch
 import torch.distributed as dist
 
+import os
+
 from . import native
 from .plan import ExecPlan, Mesh
 from .schedule import Program
@@ -41,6 +43,9 @@ class Group:
         return self.local[global_rank]
 
 
+PREFETCH = os.environ.get("MPEXEC_PREFETCH_RELAYOUT", "0") == "1"
+
+
 class Comm:
     def __init__(self, plan: ExecPlan, program: Program, rank: int, world: int):
         self.rank = rank
@@ -55,16 +60,19 @@ class Comm:
         for st in plan.stages:
             m = st.mesh
             if m.size > 1:
-                keys.append(("stage", st.index, tuple(sorted(m.device_ids))))
-                for axes in ((0,), (1,), (0, 1)):
-                    if m.group_extent(axes) <= 1:
-                        continue
-                    seen = set()
-                    for d in m.device_ids:
-                        grp = m.axis_group(d, axes)
-                        if grp not in seen:
-                            seen.add(grp)
-                            keys.append(("axis", st.index, axes, grp))
+                # "pf": the same groups again for relayouts prefetched on the side
+                # stream (NCCL must not see two streams driving one communicator)
+                for tag in ("", "pf-") if PREFETCH else ("",):
+                    keys.append((tag + "stage", st.index, tuple(sorted(m.device_ids))))
+                    for axes in ((0,), (1,), (0, 1)):
+                        if m.group_extent(axes) <= 1:
+                            continue
+                        seen = set()
+                        for d in m.device_ids:
+                            grp = m.axis_group(d, axes)
+                            if grp not in seen:
+                                seen.add(grp)
+                                keys.append((tag + "axis", st.index, axes, grp))
         for bd in program.boundaries:
             ranks = tuple(sorted(set(plan.stages[bd.producer].mesh.device_ids)
                                  | set(plan.stages[bd.consumer].mesh.device_ids)))
@@ -112,11 +120,14 @@ class Comm:
                              [(buf[self.world + i:self.world + i + 1], i) for i in peers])
         torch.cuda.synchronize()
 
-    def stage_group(self, st_index: int, mesh: Mesh) -> Group:
-        return self._groups[("stage", st_index, tuple(sorted(mesh.device_ids)))]
+    def stage_group(self, st_index: int, mesh: Mesh, pf: bool = False) -> Group:
+        return self._groups[("pf-stage" if pf else "stage", st_index,
+                             tuple(sorted(mesh.device_ids)))]
 
-    def axis_group(self, st_index: int, mesh: Mesh, axes: tuple[int, ...], device: int) -> Group:
-        return self._groups[("axis", st_index, axes, mesh.axis_group(device, axes))]
+    def axis_group(self, st_index: int, mesh: Mesh, axes: tuple[int, ...], device: int,
+                   pf: bool = False) -> Group:
+        return self._groups[("pf-axis" if pf else "axis", st_index, axes,
+                             mesh.axis_group(device, axes))]
 
     def boundary_group(self, bd, plan: ExecPlan) -> Group:
         ranks = tuple(sorted(set(plan.stages[bd.producer].mesh.device_ids)

@@ -141,6 +141,11 @@ BUSY_OPS = ("compute", "send", "all_gather")      # sim.py:23
 # is a deadlock (ExecError naming the first unfinished instruction)
 STEP_TIMEOUT_S = float(os.environ.get("MPEXEC_STEP_TIMEOUT_S", "600"))
 
+# Relayout prefetch on a side stream (StageRunner._prefetch).  Off by default:
+# measured slower on both tensor-parallel bench plans (gpt13b_n4_tp 3149 -> 3011,
+# moe24b_n4_ep 866 -> 801 TFLOP/s): the side-stream NCCL kernels take SMs from
+# the persistent GEMMs that overlap them.
+PREFETCH_RELAYOUT = os.environ.get("MPEXEC_PREFETCH_RELAYOUT", "0") == "1"
 GATHER_ANY_DIM = os.environ.get("MPEXEC_GATHER_ANY_DIM", "1") != "0"
 FUSE_BMM_EPI = os.environ.get("MPEXEC_FUSE_BMM_EPILOGUE", "1") == "1"
 
@@ -208,7 +213,14 @@ class StageRunner:
         # MPEXEC_OP_TIMING=1: CUDA events around every op and relayout (analysis only)
         self.op_timer = [] if os.environ.get("MPEXEC_OP_TIMING") == "1" else None
         self.relayout_timer: list = []
+        # relayout prefetch (see _prefetch): learned (node -> layouts its consumers
+        # reshard it to), issued on a side stream as soon as the node is produced
+        self._pf = False
+        self.pf_stream = None
+        self.pf_learn: dict[int, list] = {}
         self._compile()
+        if self.mesh.size > 1 and PREFETCH_RELAYOUT:
+            self.pf_stream = torch.cuda.Stream()
         self._init_params(params)
         self.step_count = 0
         self.vals: dict[int, dict[int, torch.Tensor]] = {}
@@ -728,7 +740,8 @@ class StageRunner:
             out = torch.empty(local_dims(dims, req, self.mesh), dtype=v.dtype, device=self.dev)
             src = self._contig(self._as3(v))
             self.comm.all_gather_into(out.view(-1), src.view(-1),
-                                      self.comm.axis_group(self.st.index, self.mesh, info, self.me))
+                                      self.comm.axis_group(self.st.index, self.mesh, info, self.me,
+                                                           pf=self._pf))
             return out
         if kind == "allgather_dim":
             # gather into a (g, *tile) staging buffer, then one copy that moves
@@ -738,7 +751,8 @@ class StageRunner:
             g = self.mesh.group_extent(axes)
             stage = torch.empty((g,) + tuple(src.shape), dtype=v.dtype, device=self.dev)
             self.comm.all_gather_into(stage.view(-1), src.view(-1),
-                                      self.comm.axis_group(self.st.index, self.mesh, axes, self.me))
+                                      self.comm.axis_group(self.st.index, self.mesh, axes, self.me,
+                                                           pf=self._pf))
             perm = stage.movedim(0, d)
             return native.pack_box(perm, (0,) * perm.dim(), tuple(perm.shape)).view(
                 *local_dims(dims, req, self.mesh))
@@ -879,11 +893,55 @@ class StageRunner:
             return v
         key = (nid, req)
         c = self.cache.setdefault(mb, {})
-        if key in c:
-            return c[key]
+        hit = c.get(key)
+        if hit is not None:
+            if type(hit) is tuple:                 # prefetched on the side stream
+                t, ev = hit
+                cur = torch.cuda.current_stream()
+                cur.wait_event(ev)
+                t.record_stream(cur)
+                c[key] = t
+                return t
+            return hit
         out = self._coerce(v, self.graph[nid].dims, have, req)
         c[key] = out
+        if self.pf_stream is not None and not self.use_graphs:
+            dims = tuple(self.graph[nid].dims)
+            if self._relayout_plan(dims, canonical(have, self.mesh),
+                                   canonical(req, self.mesh))[0] != "local":
+                reqs = self.pf_learn.setdefault(nid, [])
+                if req not in reqs:
+                    reqs.append(req)
         return out
+
+    def _prefetch(self, mb: int, nid: int) -> None:
+        """Issue the relayouts node `nid`'s consumers needed last time (learned
+        by get) right after it is produced, on the side stream with its own
+        communicators, so the transfer overlaps the ops in between; get() then
+        only waits on the event.  Every rank of the stage issues the same
+        prefetches in the same order (same program, same learned table)."""
+        v = self.vals[mb].get(nid)
+        if v is None:
+            return
+        c = self.cache.setdefault(mb, {})
+        have = self.have_spec(nid)
+        dims = self.graph[nid].dims
+        cur = torch.cuda.current_stream()
+        for req in self.pf_learn[nid]:
+            key = (nid, req)
+            if key in c or req == have:
+                continue
+            self.pf_stream.wait_stream(cur)
+            self._pf = True
+            try:
+                with torch.cuda.stream(self.pf_stream):
+                    out = self._coerce(v, dims, have, req)
+                    ev = torch.cuda.Event()
+                    ev.record(self.pf_stream)
+            finally:
+                self._pf = False
+            v.record_stream(self.pf_stream)
+            c[key] = (out, ev)
 
     def _relayout_plan(self, dims, have: Spec, req: Spec):
         """How to realise `req` from `have` on this mesh (cached; decided from
@@ -955,7 +1013,7 @@ class StageRunner:
                                                                 device=self.dev)
                 recvs.append((buf, mv.src, lo, ext, view is None))
         if sends or recvs:
-            grp = self.comm.stage_group(self.st.index, self.mesh)
+            grp = self.comm.stage_group(self.st.index, self.mesh, pf=self._pf)
             works = self.comm.p2p(sends, [(b, s) for b, s, *_ in recvs], grp)
             for w in works:
                 w.wait()
@@ -1291,6 +1349,7 @@ class StageRunner:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record()
                 r0 = len(self.relayout_timer)
+            n_before = len(vals)
             try:
                 if op.op == "input":
                     if skip_inputs:
@@ -1314,6 +1373,11 @@ class StageRunner:
                                 f"{op.nid} ({op.op}): {e}", kind="kernel") from None
             if out is not None:
                 vals[op.nid] = out
+            if self.pf_learn and not skip_inputs and len(vals) > n_before:
+                it = reversed(vals)
+                for nid in [next(it) for _ in range(len(vals) - n_before)]:
+                    if nid in self.pf_learn:
+                        self._prefetch(mb, nid)
             if timer is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record()
@@ -1613,6 +1677,8 @@ class StageRunner:
                 events.append((ins, e0, e1))
             markers.append((ins, e1))
         self.join_dw()
+        if self.pf_stream is not None:
+            stream.wait_stream(self.pf_stream)
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(stream)
         return t0, t1, events, markers

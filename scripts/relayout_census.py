@@ -28,6 +28,7 @@ def census(plan_path, device):
     r.cons = plan.graph.consumers()
     r._moves_cache, r._plans = {}, {}
     r.op_timer, r.relayout_timer = None, []
+    r._pf, r.pf_stream, r.pf_learn = False, None, {}
     r._compile()
     rows = Counter()
     nbytes = Counter()
