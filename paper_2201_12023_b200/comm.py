@@ -19,13 +19,12 @@ Group ranks are ordered by global device id (= NCCL rank order).
 """
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
 import torch
 import torch.distributed as dist
-
-import os
 
 from . import native
 from .plan import ExecPlan, Mesh
