@@ -235,7 +235,7 @@ class StageRunner:
         self.send_stream = torch.cuda.Stream()
         self.sends_pending = False
         # CUDA graphs: one capture per (phase, slot); slots = in-flight bound
-        self.use_graphs = os.environ.get("MPEXEC_CUDA_GRAPHS", "0") == "1"
+        self.use_graphs = os.environ.get("MPEXEC_CUDA_GRAPHS", "1") == "1"
         nst = len(plan.stages)
         B = plan.num_microbatches
         self.n_slots = (max(1, min(B, nst - self.st.index)) if program.schedule == "1f1b" or
@@ -246,6 +246,13 @@ class StageRunner:
         self.static: dict = {}
         self.slot_send_ev: dict[int, torch.cuda.Event] = {}
         self.cap_out: dict = {}
+        self.cap_routes: dict = {}
+        self.graph_kernels: dict = {}
+        self.replayed_kernels = 0        # libmpexec kernels launched by graph replays
+        self._cap_routes: list = []
+        bwd = [i.microbatch for i in self.sprog.instructions
+               if i.op == "compute" and i.phase == "bwd"]
+        self.first_bwd_mb = bwd[0] if bwd else None
 
         self.input_mode = "host" if host_inputs else ("fn" if inputs is not None else "resident")
         self._resident_inputs: dict = {}
@@ -1144,7 +1151,10 @@ class StageRunner:
             route = native.moe_route(gates, S, C)
             y = native.moe_mask(route, gates, S, C, 0 if kind == "dispatch" else 1)
             if self.keep_outputs and kind == "dispatch":
-                self.routes[(mb, op.ins[0][0])] = route.cpu().numpy()
+                if torch.cuda.is_current_stream_capturing():
+                    self._cap_routes.append((op.ins[0][0], route))   # copied after replays
+                else:
+                    self.routes[(mb, op.ins[0][0])] = route.cpu().numpy()
         elif kind in ("dispatch_grad", "combine_grad"):
             G, S, E, C = op.bound.route
             gates = self._contig(self.get(mb, op.ins[1][0], op.ins[1][1]))
@@ -1316,7 +1326,10 @@ class StageRunner:
         self._slot_guard(mb)
         if phase == "fwd":
             self._graph_inputs(mb)
-        key = (phase, self.slot_of(mb))
+        # the step's first backward overwrites the fp32 gradient buffers (beta = 0)
+        # and the others accumulate, so it replays a graph of its own
+        first = phase == "bwd" and mb == self.first_bwd_mb
+        key = (phase, self.slot_of(mb), first)
         vals = self.vals.setdefault(mb, {})
         g = self.graphs.get(key)
         if g is None:
@@ -1324,12 +1337,19 @@ class StageRunner:
             g = torch.cuda.CUDAGraph()
             self.join_dw()
             had_out = mb in self.outputs
+            self.g_fresh = set(self.gviews) if first else set()
+            self._cap_routes = []
+            l0 = native.launch_count()
             with torch.cuda.graph(g):
                 self._compute_eager(phase, mb, skip_inputs=True)
                 self.join_dw()
+            # libmpexec kernels in the graph: every replay launches them again
+            self.graph_kernels[key] = native.launch_count() - l0
+            self.g_fresh = set()
             self.graphs[key] = g
             self.cap_vals[key] = {n: v for n, v in vals.items() if n not in before}
             self.cap_aux[key] = dict(self.aux.get(mb, {}))
+            self.cap_routes[key] = self._cap_routes
             if self.keep_outputs and not had_out and mb in self.outputs:
                 self.cap_out[key] = self.outputs[mb]      # the slot's static output buffer
             g.replay()
@@ -1338,8 +1358,11 @@ class StageRunner:
             if self.cap_aux[key]:
                 self.aux.setdefault(mb, {}).update(self.cap_aux[key])
             g.replay()
+            self.replayed_kernels += self.graph_kernels[key]
         if key in self.cap_out:            # a replay rewrites the buffer: keep a copy
             self.outputs[mb] = self.cap_out[key].clone()
+        for gid, route in self.cap_routes.get(key, ()):
+            self.routes[(mb, gid)] = route.cpu().numpy()
 
     def _compute_eager(self, phase: str, mb: int, skip_inputs: bool = False):
         vals = self.vals.setdefault(mb, {})
@@ -1585,18 +1608,10 @@ class StageRunner:
 
     def zero_grads(self):
         self.join_dw()
-        if not self.use_graphs:
-            # every dW GEMM's first launch of the step runs with beta = 0; the
-            # gradbuf regions no dW writes stay at their initial zeros
-            self.g_fresh = set(self.gviews)
-            return
-        # a captured backward replays one fixed beta: keep the explicit fill
-        self.g_fresh = set()
-        self.gradbuf.zero_()
-        for dw, gv in self.gviews.items():
-            if gv.data_ptr() < self.gradbuf.data_ptr() or \
-                    gv.data_ptr() >= self.gradbuf.data_ptr() + self.gradbuf.numel() * 4:
-                gv.zero_()
+        # every dW GEMM's first launch of the step runs with beta = 0 (graph mode:
+        # the first backward's own graph was captured that way); the gradbuf
+        # regions no dW writes stay at their initial zeros
+        self.g_fresh = set() if self.use_graphs else set(self.gviews)
 
     def local_grad(self, pid: int) -> torch.Tensor:
         """This device's tile of pid's reduced gradient (after reduce_grads)."""
