@@ -248,6 +248,7 @@ class StageRunner:
         self.cap_out: dict = {}
         self.cap_routes: dict = {}
         self.graph_kernels: dict = {}
+        self.capture_stream = None
         self.replayed_kernels = 0        # libmpexec kernels launched by graph replays
         self._cap_routes: list = []
         bwd = [i.microbatch for i in self.sprog.instructions
@@ -1340,9 +1341,8 @@ class StageRunner:
             self.g_fresh = set(self.gviews) if first else set()
             self._cap_routes = []
             l0 = native.launch_count()
-            with torch.cuda.graph(g):
-                self._compute_eager(phase, mb, skip_inputs=True)
-                self.join_dw()
+            self._capture(g, lambda: (self._compute_eager(phase, mb, skip_inputs=True),
+                                      self.join_dw()))
             # libmpexec kernels in the graph: every replay launches them again
             self.graph_kernels[key] = native.launch_count() - l0
             self.g_fresh = set()
@@ -1363,6 +1363,24 @@ class StageRunner:
             self.outputs[mb] = self.cap_out[key].clone()
         for gid, route in self.cap_routes.get(key, ()):
             self.routes[(mb, gid)] = route.cpu().numpy()
+
+    def _capture(self, g: "torch.cuda.CUDAGraph", fn) -> None:
+        """Capture fn() into g on a side stream.  Unlike torch.cuda.graph() this
+        does not synchronize the device first: a capture in a step whose
+        peer never sends would otherwise block the host, and the step watchdog
+        could not report the deadlock."""
+        cur = torch.cuda.current_stream()
+        if self.capture_stream is None:
+            self.capture_stream = torch.cuda.Stream()
+        cs = self.capture_stream
+        cs.wait_stream(cur)
+        with torch.cuda.stream(cs):
+            g.capture_begin(capture_error_mode="thread_local")
+            try:
+                fn()
+            finally:
+                g.capture_end()
+        cur.wait_stream(cs)
 
     def _compute_eager(self, phase: str, mb: int, skip_inputs: bool = False):
         vals = self.vals.setdefault(mb, {})
