@@ -174,8 +174,10 @@ __global__ void __launch_bounds__(192, 2)
   uint64_t* v_empty = bars + 6;
   uint64_t* s_full = bars + 7;
   uint64_t* s_free = bars + 8;
-  uint64_t* p_full = bars + 9;
+  uint64_t* p_full = bars + 9;     // P keys 0-63 in smem (4 softmax warps)
   uint64_t* o_done = bars + 10;
+  uint64_t* p_full1 = bars + 14;   // P keys 64-127 in smem
+  uint64_t* p0_free = bars + 15;   // PV has read P keys 0-63 (first four K steps done)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -200,6 +202,8 @@ __global__ void __launch_bounds__(192, 2)
     mbar_init(s_full, 1);
     mbar_init(s_free, 4);
     mbar_init(p_full, 4);
+    mbar_init(p_full1, 4);
+    mbar_init(p0_free, 1);
     mbar_init(o_done, 1);
     fence_barrier_init();
   }
@@ -246,14 +250,23 @@ __global__ void __launch_bounds__(192, 2)
       issue_s(0);
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) issue_s(j + 1);
-        mbar_wait(p_full, j & 1);
         mbar_wait(v_full, j & 1);
-        tc_fence_after();
+        // O += P V in two halves of 64 keys: the first half starts as soon as the
+        // softmax warps have written P's first 64 keys, and its completion
+        // (p0_free) lets them write the next tile's first half while the
+        // second half still runs
 #pragma unroll
-        for (int kk = 0; kk < FA_BN / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(p_base + (kk >> 2) * FA_TILE + (kk & 3) * 32, 16, 1024);
-          const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, 8192, 1024);
-          tc_mma_f16(tO, ad, bd, id_o, (j | kk) != 0);
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(h ? p_full1 : p_full, j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = h * 4 + k4;
+            const uint64_t ad = umma_desc_sw128(p_base + h * FA_TILE + k4 * 32, 16, 1024);
+            const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, 8192, 1024);
+            tc_mma_f16(tO, ad, bd, id_o, (j | kk) != 0);
+          }
+          if (h == 0) tc_commit(p0_free);
         }
         tc_commit(v_empty);
         tc_commit(o_done);
@@ -291,11 +304,14 @@ __global__ void __launch_bounds__(192, 2)
         alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
         m_used = mx;
       }
-      // P must not overwrite smem before PV_{j-1} has consumed it
+      // P must not overwrite smem before PV_{j-1} has consumed it: the first half
+      // once PV_{j-1}'s first four K steps are done, the second once all are
+      // (a rescale of O needs the whole PV_{j-1} first)
+      const bool any_need = __any_sync(0xffffffffu, need);
       if (j > 0) {
-        mbar_wait(o_done, (j - 1) & 1);
+        mbar_wait(any_need ? o_done : p0_free, (j - 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, need)) {
+        if (any_need) {
 #pragma unroll 1
           for (int c = 0; c < 2; ++c) {
             uint32_t o32[32];
@@ -323,6 +339,17 @@ __global__ void __launch_bounds__(192, 2)
       uint64_t sum2 = f2pack(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
+        if (c == 2) {
+          // first 64 keys of P are in smem: PV's first half may start
+          fence_async_smem();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_full);
+          if (j > 0 && !any_need) {
+            mbar_wait(o_done, (j - 1) & 1);
+            tc_fence_after();
+          }
+        }
         const uint32_t(&t32)[32] = sv[c];
         uint8_t* chunk = sP + (c >> 1) * FA_TILE;
 #pragma unroll
@@ -348,7 +375,7 @@ __global__ void __launch_bounds__(192, 2)
       fence_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(p_full1);
     }
     // epilogue
     mbar_wait(o_done, (n_kv - 1) & 1);
