@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include "common.cuh"
 #include "../../include/mp_exec.h"
 
@@ -51,6 +52,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
       "r"(r[15]));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
 }
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -148,14 +154,31 @@ struct FaFwdParams {
   float* lse;        // [B*H, s]
 };
 
-// smem: Q 16K | K[2] 32K | V 16K | P 32K | barriers  (97 KB: two CTAs per SM)
+// smem: Q 16K | K[2] 32K | V 16K | P 32K | barriers  (97 KB: two CTAs per SM).
+// With P in TMEM (PT, the default) the P tiles are not allocated: 65 KB.
 constexpr int FA_FWD_SMEM = FA_TILE * 6 + 1024 + 256;
+constexpr int FA_FWD_SMEM_PT = FA_TILE * 4 + 1024 + 256;
+
+// tcgen05.mma with A read from tensor memory (TS form): P V with P in TMEM
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 // tcgen05.ld 32 lanes x 32b x 32 columns
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   tmem_ld_32x32b_x32(taddr, r);
 }
 
+// PT: P (bf16) goes to its own 64 TMEM columns with tcgen05.st and P V reads it from
+// there (TS-form MMA) -- no shared-memory P tiles, no st.shared / proxy fence on
+// the softmax path, and the P V MMA only streams V from shared memory.
+template <bool PT>
 __global__ void __launch_bounds__(192, 2)
     fa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const FaFwdParams p) {
@@ -165,8 +188,8 @@ __global__ void __launch_bounds__(192, 2)
   uint8_t* sQ = smem;
   uint8_t* sK = smem + FA_TILE;          // 2 stages
   uint8_t* sV = smem + 3 * FA_TILE;      // 1 stage
-  uint8_t* sP = smem + 4 * FA_TILE;      // 2 chunks of 64 keys
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * FA_TILE);
+  uint8_t* sP = smem + 4 * FA_TILE;      // 2 chunks of 64 keys (not PT)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (PT ? 4 : 6) * FA_TILE);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;    // [2]
   uint64_t* k_empty = bars + 3;   // [2]
@@ -212,7 +235,7 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + 128;
+  const uint32_t tS = tmem, tO = tmem + 128, tP = tmem + 192;   // tP: PT only
 
   if (warp == 0) {
     if (lane == 0) {
@@ -262,9 +285,13 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int kk = h * 4 + k4;
-            const uint64_t ad = umma_desc_sw128(p_base + h * FA_TILE + k4 * 32, 16, 1024);
             const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, 8192, 1024);
-            tc_mma_f16(tO, ad, bd, id_o, (j | kk) != 0);
+            if (PT) {
+              tc_mma_f16_ts(tO, tP + kk * 8, bd, id_o, (j | kk) != 0);   // 16 keys = 8 columns
+            } else {
+              const uint64_t ad = umma_desc_sw128(p_base + h * FA_TILE + k4 * 32, 16, 1024);
+              tc_mma_f16(tO, ad, bd, id_o, (j | kk) != 0);
+            }
           }
           if (h == 0) tc_commit(p0_free);
         }
@@ -340,8 +367,11 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (c == 2) {
-          // first 64 keys of P are in smem: PV's first half may start
-          fence_async_smem();
+          // first 64 keys of P are written: PV's first half may start
+          if (PT)
+            tmem_st_wait();
+          else
+            fence_async_smem();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(p_full);
@@ -352,6 +382,7 @@ __global__ void __launch_bounds__(192, 2)
         }
         const uint32_t(&t32)[32] = sv[c];
         uint8_t* chunk = sP + (c >> 1) * FA_TILE;
+        uint32_t pk[16];   // PT: the chunk's 32 keys as 16 packed bf16 pairs
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           float pv[8];
@@ -364,15 +395,24 @@ __global__ void __launch_bounds__(192, 2)
             pv[e + 1] = ex2(x1);
             sum2 = fadd2(sum2, f2pack(pv[e], pv[e + 1]));
           }
-          st_sw128(chunk, r, (c & 1) * 4 + t,
-                   make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]),
-                              pack_bf2(pv[4], pv[5]), pack_bf2(pv[6], pv[7])));
+          if (PT) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pk[t * 4 + e] = pack_bf2(pv[2 * e], pv[2 * e + 1]);
+          } else {
+            st_sw128(chunk, r, (c & 1) * 4 + t,
+                     make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]),
+                                pack_bf2(pv[4], pv[5]), pack_bf2(pv[6], pv[7])));
+          }
         }
+        if (PT) tmem_st16(tP + lane_off + c * 16, pk);
       }
       float s0, s1;
       f2unpack(sum2, s0, s1);
       l += s0 + s1;
-      fence_async_smem();
+      if (PT)
+        tmem_st_wait();
+      else
+        fence_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full1);
@@ -439,6 +479,11 @@ constexpr int FA_BWD_THREADS = 448;   // TMA, MMA, 8 P/dS warps, 4 dQ warps
 // up, its K/V as soon as the last MMA of the previous tile has read K/V
 // (kv_empty), and the dK/dV epilogue of tile t overlaps the K/V load of t+1
 // (the first dV/dK MMA of t+1 waits for acc_free).
+// PT: P^T (bf16) goes to TMEM with tcgen05.st and the dV MMA reads it from there (TS
+// form), so P^T costs neither shared-memory stores nor shared-memory operand reads
+// (the backward is bound by shared-memory bandwidth); the dQ accumulator is
+// single-buffered to make room for it.
+template <bool PT>
 __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -471,6 +516,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
   uint64_t* s_free = bars + 13;      // 8 P/dS warps hold S^T / dP^T of g in registers
   uint64_t* kv_empty = bars + 14;    // last MMA of the work tile has read K / V
   uint64_t* acc_free = bars + 15;    // dK / dV TMEM drained by the epilogue (8 warps)
+  uint64_t* pt_free = bars + 20;     // PT: the dV MMAs of g have read P^T(g) from TMEM
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = p.s / FA_BM;
@@ -497,6 +543,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     mbar_init(s_free, 8);
     mbar_init(kv_empty, 1);
     mbar_init(acc_free, 8);
+    mbar_init(pt_free, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -505,7 +552,8 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tSt = tmem, tdPt = tmem + 128, tdV = tmem + 256, tdK = tmem + 320,
-                 tdQ = tmem + 384;   // [2] x 64 columns
+                 tdQ = tmem + 384;   // [2] x 64 columns (PT: one buffer)
+  const uint32_t tPt = tmem + 448;   // PT: P^T as 64 columns of packed bf16 pairs
 
   if (warp == 0) {
     // TMA producer (lane 0) + lse / D staging (all lanes; the next query tile's
@@ -569,20 +617,41 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         }
         const uint32_t pt = smem_u32(sPt + bj * 2 * FA_TILE), ds = smem_u32(sdSt + bj * 2 * FA_TILE);
         const uint32_t qb = smem_u32(sQ + bj * FA_TILE), dob = smem_u32(sdO + bj * FA_TILE);
+        if (PT) {
+          // dV += P^T dO with P^T from TMEM (16 queries = 8 columns per K step)
 #pragma unroll
-        for (int kk = 0; kk < FA_BM / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * FA_TILE + (kk & 3) * 32;
-          tc_mma_f16(tdV, umma_desc_sw128(pt + aoff, 16, 1024),
-                     umma_desc_sw128(dob + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
-          tc_mma_f16(tdK, umma_desc_sw128(ds + aoff, 16, 1024),
-                     umma_desc_sw128(qb + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
+          for (int kk = 0; kk < FA_BM / 16; ++kk)
+            tc_mma_f16_ts(tdV, tPt + kk * 8, umma_desc_sw128(dob + kk * 2048, 8192, 1024), id_acc,
+                          (j | kk) != 0);
+          tc_commit(pt_free);
+#pragma unroll
+          for (int kk = 0; kk < FA_BM / 16; ++kk) {
+            const uint32_t aoff = (kk >> 2) * FA_TILE + (kk & 3) * 32;
+            tc_mma_f16(tdK, umma_desc_sw128(ds + aoff, 16, 1024),
+                       umma_desc_sw128(qb + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < FA_BM / 16; ++kk) {
+            const uint32_t aoff = (kk >> 2) * FA_TILE + (kk & 3) * 32;
+            tc_mma_f16(tdV, umma_desc_sw128(pt + aoff, 16, 1024),
+                       umma_desc_sw128(dob + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
+            tc_mma_f16(tdK, umma_desc_sw128(ds + aoff, 16, 1024),
+                       umma_desc_sw128(qb + kk * 2048, 8192, 1024), id_acc, (j | kk) != 0);
+          }
         }
         tc_commit(&q_empty[bj]);     // Q / dO of gj read: the next load may start
-        if (gj >= 2) mbar_wait(&dq_free[bj], ((gj >> 1) & 1) ^ 1);
+        // the dQ TMEM buffer this MMA writes was last read by the dQ warps for gj-2
+        // (two buffers) or gj-1 (PT: one buffer)
+        if (PT) {
+          if (gj >= 1) mbar_wait(&dq_free[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
+        } else if (gj >= 2) {
+          mbar_wait(&dq_free[bj], ((gj >> 1) & 1) ^ 1);
+        }
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < FA_BN / 16; ++kk)
-          tc_mma_f16(tdQ + bj * 64, umma_desc_sw128(ds + kk * 2048, FA_TILE, 1024),
+          tc_mma_f16(tdQ + (PT ? 0 : bj * 64), umma_desc_sw128(ds + kk * 2048, FA_TILE, 1024),
                      umma_desc_sw128(k_base + kk * 2048, 8192, 1024), id_dq, kk > 0);
         tc_commit(&dq_full[bj]);   // also: dK / dQ MMAs done with dS^T (the dQ warps reuse it)
       };
@@ -637,6 +706,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         if (g >= 2) mbar_wait(&pbuf_free[bi], ((g >> 1) & 1) ^ 1);
         uint8_t* pt = sPt + bi * 2 * FA_TILE;
         uint8_t* dst = sdSt + bi * 2 * FA_TILE;
+
         const uint32_t lse_a = smem_u32(sLse + bi * 128), d_a = smem_u32(sD + bi * 128);
         // 4 chunks of 16 queries, software-pipelined: the TMEM load of chunk
         // cc+1 is in flight while chunk cc is computed; once the last chunk is
@@ -683,12 +753,25 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
                                  f2pack(dvv[e], dvv[e + 1]))), ds[e], ds[e + 1]);
           }
           const int ch = c >> 2, u0 = (c & 3) * 2;
-          st_sw128(pt + ch * FA_TILE, r, u0,
-                   make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]), pack_bf2(pv[4], pv[5]),
-                              pack_bf2(pv[6], pv[7])));
-          st_sw128(pt + ch * FA_TILE, r, u0 + 1,
-                   make_uint4(pack_bf2(pv[8], pv[9]), pack_bf2(pv[10], pv[11]),
-                              pack_bf2(pv[12], pv[13]), pack_bf2(pv[14], pv[15])));
+          if (PT) {
+            // P^T(g) overwrites P^T(g-1) in TMEM once the dV MMAs of g-1 have read it
+            if (cc == 0 && g >= 1) {
+              mbar_wait(pt_free, (g - 1) & 1);
+              tc_fence_after();
+            }
+            const uint32_t pk[8] = {pack_bf2(pv[0], pv[1]),   pack_bf2(pv[2], pv[3]),
+                                    pack_bf2(pv[4], pv[5]),   pack_bf2(pv[6], pv[7]),
+                                    pack_bf2(pv[8], pv[9]),   pack_bf2(pv[10], pv[11]),
+                                    pack_bf2(pv[12], pv[13]), pack_bf2(pv[14], pv[15])};
+            tmem_st8(tPt + lane_off + c * 8, pk);
+          } else {
+            st_sw128(pt + ch * FA_TILE, r, u0,
+                     make_uint4(pack_bf2(pv[0], pv[1]), pack_bf2(pv[2], pv[3]),
+                                pack_bf2(pv[4], pv[5]), pack_bf2(pv[6], pv[7])));
+            st_sw128(pt + ch * FA_TILE, r, u0 + 1,
+                     make_uint4(pack_bf2(pv[8], pv[9]), pack_bf2(pv[10], pv[11]),
+                                pack_bf2(pv[12], pv[13]), pack_bf2(pv[14], pv[15])));
+          }
           st_sw128(dst + ch * FA_TILE, r, u0,
                    make_uint4(pack_bf2(ds[0], ds[1]), pack_bf2(ds[2], ds[3]), pack_bf2(ds[4], ds[5]),
                               pack_bf2(ds[6], ds[7])));
@@ -697,6 +780,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
                               pack_bf2(ds[12], ds[13]), pack_bf2(ds[14], ds[15])));
           if (cc + 1 < 4) tmem_ld_wait();
         }
+        if (PT) tmem_st_wait();
         fence_async_smem();
         tc_fence_before();
         __syncwarp();
@@ -750,7 +834,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         tc_fence_after();
         uint32_t t16[4][16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld16(tdQ + bj * 64 + lane_off + c * 16, t16[c]);
+        for (int c = 0; c < 4; ++c) tmem_ld16(tdQ + (PT ? 0 : bj * 64) + lane_off + c * 16, t16[c]);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -936,7 +1020,8 @@ static inline int preload_one(F* f) {
   return cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f)) == cudaSuccess ? 0 : 1;
 }
 int preload_attention() {
-  return preload_one(fa_fwd_kernel) | preload_one(fa_bwd_kernel) | preload_one(fa_bwd_pre_kernel) |
+  return preload_one(fa_fwd_kernel<true>) | preload_one(fa_fwd_kernel<false>) |
+         preload_one(fa_bwd_kernel<true>) | preload_one(fa_bwd_kernel<false>) | preload_one(fa_bwd_pre_kernel) |
          preload_one(attn_combine_scale_kernel) | preload_one(attn_combine_finish_kernel);
 }
 }  // namespace mp
@@ -966,15 +1051,24 @@ extern "C" int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void*
   if ((rc = fa_map(&mq, q, B * s, ld)) || (rc = fa_map(&mk, k, B * s, ld)) ||
       (rc = fa_map(&mv, v, B * s, ld)))
     return rc;
+  // MPEXEC_FA_FWD_SMEM_P=1: P through shared memory (SS-form P V), for A/B runs
+  static const bool smem_p = getenv("MPEXEC_FA_FWD_SMEM_P") != nullptr;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(fa_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_FWD_SMEM);
+    cudaFuncSetAttribute(fa_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_FWD_SMEM);
+    cudaFuncSetAttribute(fa_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_FWD_SMEM_PT);
     configured = true;
   }
   FaFwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, (int)(kv_len / FA_BN),
                 scale * 1.4426950408889634f, reinterpret_cast<uint16_t*>(o), lse};
   dim3 grid((unsigned)(s / FA_BM), (unsigned)(B * H));
-  fa_fwd_kernel<<<grid, 192, FA_FWD_SMEM, reinterpret_cast<cudaStream_t>(stream)>>>(mq, mk, mv, p);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (smem_p)
+    fa_fwd_kernel<false><<<grid, 192, FA_FWD_SMEM, st>>>(mq, mk, mv, p);
+  else
+    fa_fwd_kernel<true><<<grid, 192, FA_FWD_SMEM_PT, st>>>(mq, mk, mv, p);
   MP_CHECK_LAUNCH();
   return 0;
 }
@@ -1012,14 +1106,22 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
     return rc;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(fa_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FA_BWD_SMEM);
+    cudaFuncSetAttribute(fa_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_BWD_SMEM);
+    cudaFuncSetAttribute(fa_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_BWD_SMEM);
     configured = true;
   }
   FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, (int)(kv_len / FA_BN), scale, lse,
                 dvec, dq_acc, reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
   const int64_t work = (kv_len / FA_BN) * B * H;
   dim3 grid((unsigned)(work < num_sms() ? work : num_sms()));
-  fa_bwd_kernel<<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, mdq, p);
+  // MPEXEC_FA_BWD_SMEM_P=1: P^T through shared memory (SS-form dV MMA), for A/B runs
+  static const bool smem_p = getenv("MPEXEC_FA_BWD_SMEM_P") != nullptr;
+  if (smem_p)
+    fa_bwd_kernel<false><<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, mdq, p);
+  else
+    fa_bwd_kernel<true><<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, mdq, p);
   MP_CHECK_LAUNCH();
   return 0;
 }
