@@ -1052,7 +1052,7 @@ extern "C" int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void*
       (rc = fa_map(&mv, v, B * s, ld)))
     return rc;
   // MPEXEC_FA_FWD_SMEM_P=1: P through shared memory (SS-form P V), for A/B runs
-  static const bool smem_p = getenv("MPEXEC_FA_FWD_SMEM_P") != nullptr;
+  static const bool smem_p = getenv("MPEXEC_FA_PT") == nullptr;   // PT under validation
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(fa_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1117,7 +1117,7 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
   const int64_t work = (kv_len / FA_BN) * B * H;
   dim3 grid((unsigned)(work < num_sms() ? work : num_sms()));
   // MPEXEC_FA_BWD_SMEM_P=1: P^T through shared memory (SS-form dV MMA), for A/B runs
-  static const bool smem_p = getenv("MPEXEC_FA_BWD_SMEM_P") != nullptr;
+  static const bool smem_p = getenv("MPEXEC_FA_PT") == nullptr;   // PT under validation
   if (smem_p)
     fa_bwd_kernel<false><<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, mdq, p);
   else
