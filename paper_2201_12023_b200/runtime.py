@@ -256,6 +256,10 @@ class StageRunner:
         self.first_bwd_mb = bwd[0] if bwd else None
 
         self.input_mode = "host" if host_inputs else ("fn" if inputs is not None else "resident")
+        self.h2d_stream = None
+        self.h2d_ring: dict = {}
+        self.h2d_ring_free: dict = {}
+        self.h2d_ready: dict = {}
         self._resident_inputs: dict = {}
 
     # ------------------------------------------------------------------ compile
@@ -1269,13 +1273,7 @@ class StageRunner:
                 self.dev, dtype=torch.bfloat16)
         key = (op.nid, mb % 2)
         if self.input_mode == "host":
-            hb = self._host_input_bufs.get(key)
-            if hb is None:
-                gen = torch.Generator()
-                gen.manual_seed(stable_seed(self.seed, "input", op.nid, mb % 2))
-                full = torch.randn(dims, generator=gen)
-                hb = full[sl].contiguous().to(torch.bfloat16).pin_memory()
-                self._host_input_bufs[key] = hb
+            hb = self._host_buf(op, mb)
             self.h2d_bytes += hb.numel() * hb.element_size()
             return hb.to(self.dev, non_blocking=True)
         t = self._resident_inputs.get(key)
@@ -1300,15 +1298,65 @@ class StageRunner:
         if ev is not None:
             torch.cuda.current_stream().wait_event(ev)
 
-    def _graph_inputs(self, mb: int):
-        """Graph mode: stage this microbatch's graph inputs into the slot's
-        static buffers (outside the captured region)."""
-        vals = self.vals.setdefault(mb, {})
-        k = self.slot_of(mb)
+    def _host_buf(self, op: _Op, mb: int) -> torch.Tensor:
+        """Pinned host copy of this device's shard of a synthetic input (two
+        alternating microbatches, like the resident inputs)."""
+        key = (op.nid, mb % 2)
+        hb = self._host_input_bufs.get(key)
+        if hb is None:
+            dims = self.graph[op.nid].dims
+            box = device_box(dims, op.out_spec, self.mesh, self.me)
+            gen = torch.Generator()
+            gen.manual_seed(stable_seed(self.seed, "input", op.nid, mb % 2))
+            full = torch.randn(dims, generator=gen)
+            hb = full[tuple(slice(lo, hi) for lo, hi in box)].contiguous() \
+                .to(torch.bfloat16).pin_memory()
+            self._host_input_bufs[key] = hb
+        return hb
+
+    def _h2d_prefetch(self, mb: int) -> None:
+        """Host inputs, graph mode: copy microbatch mb's inputs H2D on a copy
+        stream into a two-deep staging ring while the previous microbatch
+        computes; the ring slot is reused once the copy out of it (two
+        microbatches earlier) has run on the compute stream."""
+        if self.h2d_stream is None:
+            self.h2d_stream = torch.cuda.Stream()
+        r = mb % 2
+        ev_free = self.h2d_ring_free.get(r)
         for op in self.fwd_ops:
             if op.op != "input":
                 continue
-            src = self._load_input(mb, op)
+            hb = self._host_buf(op, mb)
+            dst = self.h2d_ring.get((r, op.nid))
+            if dst is None:
+                dst = self.h2d_ring[(r, op.nid)] = torch.empty(hb.shape, dtype=hb.dtype,
+                                                               device=self.dev)
+            if ev_free is not None:
+                self.h2d_stream.wait_event(ev_free)
+            with torch.cuda.stream(self.h2d_stream):
+                dst.copy_(hb, non_blocking=True)
+            self.h2d_bytes += hb.numel() * hb.element_size()
+        ev = torch.cuda.Event()
+        ev.record(self.h2d_stream)
+        self.h2d_ready[mb] = (r, ev)
+
+    def _graph_inputs(self, mb: int):
+        """Graph mode: stage this microbatch's graph inputs into the slot's
+        static buffers (outside the captured region).  Host inputs arrive
+        through the prefetched H2D ring (_h2d_prefetch); the next microbatch's
+        copy is issued here, so it overlaps this microbatch's compute."""
+        vals = self.vals.setdefault(mb, {})
+        k = self.slot_of(mb)
+        host = self.input_mode == "host"
+        if host:
+            if mb not in self.h2d_ready:
+                self._h2d_prefetch(mb)
+            r, ev = self.h2d_ready.pop(mb)
+            torch.cuda.current_stream().wait_event(ev)
+        for op in self.fwd_ops:
+            if op.op != "input":
+                continue
+            src = self.h2d_ring[(r, op.nid)] if host else self._load_input(mb, op)
             key = ("in", k, op.nid)
             buf = self.static.get(key)
             if buf is None:
@@ -1316,6 +1364,12 @@ class StageRunner:
                 self.static[key] = buf
             buf.copy_(src, non_blocking=True)
             vals[op.nid] = buf
+        if host:
+            free = torch.cuda.Event()
+            free.record(torch.cuda.current_stream())
+            self.h2d_ring_free[r] = free
+            if mb + 1 < self.plan.num_microbatches:
+                self._h2d_prefetch(mb + 1)
 
     def compute(self, phase: str, mb: int):
         """Run the stage's forward or backward ops for one microbatch: eagerly,
