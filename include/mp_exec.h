@@ -215,6 +215,10 @@ int mp_reduce_scatter(void* comm, const void* send, void* recv, int64_t recvcoun
                       int op, void* stream);
 int mp_group_start(void);
 int mp_group_end(void);
+/* All-to-all of equal chunks: chunk i (count elements) of send goes to rank i, chunk i of
+ * recv comes from rank i (one NCCL group of sends and recvs).  Replaces the modeled
+ * all_to_all of resharding_cost (sharding.py:346; collective_time, costs.py:63-73). */
+int mp_alltoall(void* comm, const void* send, void* recv, int64_t count, int dtype, void* stream);
 int mp_send(void* comm, const void* buf, int64_t count, int dtype, int peer, void* stream);
 int mp_recv(void* comm, void* buf, int64_t count, int dtype, int peer, void* stream);
 

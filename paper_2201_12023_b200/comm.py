@@ -149,6 +149,10 @@ class Comm:
                          [(t, group.peer(p)) for t, p in recvs], stream)
         return []
 
+    def all_to_all(self, out_flat: torch.Tensor, in_flat: torch.Tensor, group: Group,
+                   stream=None) -> None:
+        native.alltoall(group.comm, out_flat, in_flat, len(group.ranks), stream)
+
     def all_gather_into(self, out_flat: torch.Tensor, in_flat: torch.Tensor, group: Group,
                         stream=None) -> None:
         native.allgather(group.comm, out_flat, in_flat, stream)

@@ -123,6 +123,35 @@ int mp_reduce_scatter(void* comm, const void* send, void* recv, int64_t recvcoun
   return 0;
 }
 
+// All-to-all of equal chunks (the resharding_cost all_to_all, sharding.py:346): chunk i
+// of `send` goes to rank i, chunk i of `recv` comes from rank i, `count` elements per
+// chunk; one NCCL group of sends / recvs to every rank (NCCL has no all-to-all
+// primitive; grouped point-to-point is its documented form).
+int mp_alltoall(void* comm, const void* send, void* recv, int64_t count, int dtype, void* stream) {
+  clear_error();
+  MP_CHECK_ARG(comm && send && recv && count >= 0, "bad args");
+  if (count == 0) return 0;
+  ncclComm_t c = reinterpret_cast<ncclComm_t>(comm);
+  int n = 0;
+  MP_NCCL(ncclCommCount(c, &n));
+  const size_t eb = dtype == 0 ? 2 : (dtype == 1 ? 4 : 1);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  MP_NCCL(ncclGroupStart());
+  for (int r = 0; r < n; ++r) {
+    const ncclResult_t a = ncclSend(static_cast<const char*>(send) + (size_t)r * count * eb,
+                                    (size_t)count, nccl_dtype(dtype), r, c, st);
+    const ncclResult_t b = ncclRecv(static_cast<char*>(recv) + (size_t)r * count * eb,
+                                    (size_t)count, nccl_dtype(dtype), r, c, st);
+    if (a != ncclSuccess || b != ncclSuccess) {
+      ncclGroupEnd();
+      set_error(std::string("mp_alltoall: ") + ncclGetErrorString(a != ncclSuccess ? a : b));
+      return 1;
+    }
+  }
+  MP_NCCL(ncclGroupEnd());
+  return 0;
+}
+
 int mp_group_start(void) {
   clear_error();
   MP_NCCL(ncclGroupStart());

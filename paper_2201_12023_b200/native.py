@@ -66,6 +66,7 @@ EXPORTS = {
     "mp_reduce_scatter": ([c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
     "mp_group_start": ([], c_int),
     "mp_group_end": ([], c_int),
+    "mp_alltoall": ([c_vp, c_vp, c_vp, c_i64, c_int, c_vp], c_int),
     "mp_send": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
     "mp_recv": ([c_vp, c_vp, c_i64, c_int, c_int, c_vp], c_int),
     "mp_ilp_solve": ([c_int, ctypes.POINTER(c_int), c_i64p, c_int, ctypes.POINTER(c_int),
@@ -721,6 +722,16 @@ def group_start() -> None:
 
 def group_end() -> None:
     _check(load().mp_group_end(), "mp_group_end")
+
+
+def alltoall(comm: int, out: torch.Tensor, inp: torch.Tensor, nranks: int, stream=None) -> None:
+    """Equal-chunk all-to-all over a communicator of `nranks`: chunk i of inp goes to
+    rank i, chunk i of out comes from rank i (contiguous tensors, same numel)."""
+    if not (inp.is_contiguous() and out.is_contiguous()) or inp.numel() != out.numel() \
+            or inp.numel() % nranks or inp.dtype != out.dtype:
+        raise NativeError("alltoall needs equal contiguous tensors divisible by the group size")
+    _check(load().mp_alltoall(comm, inp.data_ptr(), out.data_ptr(), inp.numel() // nranks,
+                              _dt(inp), _stream(stream)), "mp_alltoall")
 
 
 def send_recv(comm: int, sends, recvs, stream=None) -> None:

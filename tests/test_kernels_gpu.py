@@ -336,3 +336,43 @@ def test_gemm_rejects_misaligned_batch_strides():
     with pytest.raises(native.NativeError):
         native.gemm(a, b, out, epilogue=native.EPI_ADD, aux=aux)
     torch.cuda.synchronize()
+
+
+def test_alltoall_two_ranks():
+    """mp_alltoall (resharding_cost's all_to_all, sharding.py:346) on 2 GPUs:
+    chunk i of each rank's input lands as chunk `rank` on rank i."""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+    from pathlib import Path
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = Path(__file__).resolve().parent.parent
+    code = textwrap.dedent("""
+        import os, torch, torch.distributed as dist
+        from paper_2201_12023_b200 import native
+        r = int(os.environ["LOCAL_RANK"]); torch.cuda.set_device(r)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", r))
+        uid = [native.nccl_unique_id() if r == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = native.comm_init(uid[0], 2, r)
+        x = (torch.arange(2 * 1000, device="cuda", dtype=torch.float32) + 10000 * r).to(torch.bfloat16)
+        y = torch.empty_like(x)
+        native.alltoall(comm, y, x, 2)
+        torch.cuda.synchronize()
+        want = torch.cat([(torch.arange(1000, device="cuda", dtype=torch.float32) + 1000 * r + 10000 * q)
+                          .to(torch.bfloat16) for q in range(2)])
+        assert torch.equal(y, want), (r, y[:4], want[:4])
+        native.comm_destroy(comm)
+        print("ok", r, flush=True)
+        dist.destroy_process_group()
+    """)
+    script = root / "gpurun_out" / "_alltoall_probe.py"
+    script.parent.mkdir(exist_ok=True)
+    script.write_text(code)
+    res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node=2", "--master-addr", "127.0.0.1", "--master-port",
+                          "29533", str(script)], capture_output=True, text=True, timeout=300,
+                         env={**os.environ, "PYTHONPATH": str(root)})
+    assert res.returncode == 0 and res.stdout.count("ok") == 2, res.stdout[-2000:] + res.stderr[-2000:]
