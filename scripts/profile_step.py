@@ -19,6 +19,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("plan", nargs="?", default=str(ROOT / "plans/gpt13b_n1/plan.json"))
     ap.add_argument("--mb", type=int, default=2, help="microbatches to run (override plan B)")
+    ap.add_argument("--rank", type=int, default=0, help="the rank that prints")
     args = ap.parse_args()
     doc = json.loads(Path(args.plan).read_text())
     doc["num_microbatches"] = args.mb
@@ -45,11 +46,11 @@ def main():
                 name = "gemm " + name[name.find("<"):name.find(">") + 1] if "<" in name else name
             agg[name][0] += 1
             agg[name][1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
-    if world > 1 and dist.get_rank() != 0:
+    if world > 1 and dist.get_rank() != args.rank:
         dist.barrier()
         return
     total = sum(v[1] for v in agg.values())
-    print(f"step device time {dt*1e3:.1f} ms, kernel sum {total/1e3:.1f} ms")
+    print(f"rank {args.rank}: step device time {dt*1e3:.1f} ms, kernel sum {total/1e3:.1f} ms")
     for name, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:30]:
         print(f"{us/1e3:10.2f} ms {100*us/total:6.2f}% {n:7d}  {name[:110]}")
     cpu = defaultdict(lambda: [0, 0.0])

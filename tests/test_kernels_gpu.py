@@ -376,3 +376,20 @@ def test_alltoall_two_ranks():
                           "29533", str(script)], capture_output=True, text=True, timeout=300,
                          env={**os.environ, "PYTHONPATH": str(root)})
     assert res.returncode == 0 and res.stdout.count("ok") == 2, res.stdout[-2000:] + res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("shape,lo,ext", [((8192, 1024), (4096, 512), (4096, 512)),
+                                          ((8, 300, 96), (2, 7, 8), (5, 290, 80)),
+                                          ((3, 4, 70, 64), (1, 0, 5, 8), (2, 4, 64, 56))])
+def test_pack_unpack_box_rows(shape, lo, ext):
+    """Row-form box copies (one warp per innermost row, >= 64 rows): exact on 2-, 3-
+    and 4-D boxes of strided tiles, both directions."""
+    t = torch.randn(*shape, device="cuda").to(torch.bfloat16)
+    sl = tuple(slice(a, a + e) for a, e in zip(lo, ext))
+    buf = native.pack_box(t, lo, ext)
+    assert torch.equal(buf, t[sl].reshape(-1))
+    dst = torch.zeros_like(t)
+    native.unpack_box(buf, dst, lo, ext)
+    assert torch.equal(dst[sl], t[sl])
+    dst[sl] = 0
+    assert not dst.any()
