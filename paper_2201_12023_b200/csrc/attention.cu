@@ -83,6 +83,9 @@ __device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* 
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -703,7 +706,8 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         mbar_wait(st_full, g & 1);
         tc_fence_after();
         // this P^T / dS^T buffer was last read by the MMAs of g-2
-        if (g >= 2) mbar_wait(&pbuf_free[bi], ((g >> 1) & 1) ^ 1);
+        // (PT: dQ is staged elsewhere, so the dK / dQ MMAs of g-2 are the last readers)
+        if (g >= 2) mbar_wait(PT ? &dq_full[bi] : &pbuf_free[bi], ((g >> 1) & 1) ^ 1);
         uint8_t* pt = sPt + bi * 2 * FA_TILE;
         uint8_t* dst = sdSt + bi * 2 * FA_TILE;
 
@@ -840,7 +844,12 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&dq_free[bj]);
 #ifndef MP_FA_NO_DQ_RED
-        uint8_t* stage = sdSt + bj * 2 * FA_TILE;
+        // PT: dQ is staged in the (otherwise unused) smem P^T buffers, two-deep, so the
+        // P warps never wait on the dQ reduction; the leader's wait for the TMA read of
+        // the buffer's previous use (wait_group.read 1 at the end of the last
+        // iteration) is published to the other dQ warps by this barrier
+        if (PT) asm volatile("bar.sync 1, 128;" ::: "memory");
+        uint8_t* stage = (PT ? sPt : sdSt) + bj * 2 * FA_TILE;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {        // columns 16c .. 16c+15: half c/2, units 4(c&1)..+3
           uint8_t* chunk = stage + (c >> 1) * FA_TILE;
@@ -860,8 +869,12 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
           tma_reduce_add_2d(&tmdQ, stage, hh * FA_D, row0 + i * FA_BM);
           tma_reduce_add_2d(&tmdQ, stage + FA_TILE, hh * FA_D + 32, row0 + i * FA_BM);
           bulk_commit();
-          bulk_wait_read0();
-          mbar_arrive(&pbuf_free[bj]);
+          if (PT) {
+            bulk_wait_read1();            // the other staging buffer has been read
+          } else {
+            bulk_wait_read0();
+            mbar_arrive(&pbuf_free[bj]);
+          }
         }
 #else
         if (leader) mbar_arrive(&pbuf_free[bj]);
