@@ -187,8 +187,8 @@ def run_reference(args):
 
 def _traffic():
     """dram read + write bytes of one GEMM launch from the committed ncu --set full
-    capture (profiles/r1_gemm_traffic.json), or None."""
-    p = ROOT / "profiles/r1_gemm_traffic.json"
+    capture (profiles/r2_gemm_traffic.json), or None."""
+    p = ROOT / "profiles/r2_gemm_traffic.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text())
