@@ -116,9 +116,12 @@ def cpu_baseline_sample(threads: int):
     x = {n["id"]: rng.standard_normal(n["shape"]["dims"], dtype=np.float32)
          for n in nodes if n["kind"] == "input"}
     flops = sum(n["flop"] for n in nodes if n["kind"] in ("matmul", "batched_matmul"))
-    t0 = time.perf_counter()
-    dense.run(doc, params, lambda mb, nid: x[nid], 1, dtype=np.float32)
-    dt = time.perf_counter() - t0
+    # torchrun exports OMP_NUM_THREADS=1 to every rank: give BLAS the host's threads back
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        dense.run(doc, params, lambda mb, nid: x[nid], 1, dtype=np.float32)
+        dt = time.perf_counter() - t0
     return flops / dt / 1e12, dt, flops
 
 
