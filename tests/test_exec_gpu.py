@@ -42,6 +42,9 @@ def test_full_size_parity(plan, fused):
     errs = run_plan(ROOT / plan, "1f1b", dtype=np.float32)
     print(json.dumps(errs))
     assert errs["ok"], errs
+    # at these shapes the fixed tolerances hold on their own (no bf16-storage widening)
+    for k in ("loss", "grad", "output", "grad_global"):
+        assert errs[k] <= TOL[k], (k, errs)
     for k, n in fused.items():
         assert errs["fused"][k] >= n, errs["fused"]
     torch.cuda.empty_cache()
