@@ -117,3 +117,28 @@ def test_deadlock_names_the_blocked_instruction():
     assert outs[1].get("kind") == "deadlock", outs
     assert outs[1]["instruction"] == "f:0>1:0", outs
     assert outs[1]["msg"].startswith("deadlock: rank 1 stage 1 waiting on recv f:0>1:0"), outs
+
+
+def test_cli_execute_two_stages(tmp_path):
+    """The CLI twin under torchrun on a 2-stage plan: rank 0 writes one sim.json with
+    both stages' utilization, both devices' peaks and every instruction of both
+    stages, and gantt rows for both devices."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=2", "--master-addr", "127.0.0.1", "--master-port",
+                        "29541", "-m", "paper_2201_12023_b200", "execute", "--plan",
+                        "plans/tiny_gpt_n2/plan.json", "--schedule", "1f1b", "--steps", "2",
+                        "--out", str(tmp_path)], capture_output=True, text=True, cwd=ROOT,
+                       env=ENV, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    doc = json.loads((tmp_path / "sim.json").read_text())
+    assert set(doc["utilization"]) == {"0", "1"} and set(doc["peak_bytes"]) == {"0", "1"}
+    from paper_2201_12023_b200.plan import load_plan
+    from paper_2201_12023_b200.runtime import _label
+    from paper_2201_12023_b200.schedule import build_program
+    prog = build_program(load_plan(ROOT / "plans/tiny_gpt_n2/plan.json"), "1f1b")
+    want = sorted((sp.stage, i.op, _label(i)) for sp in prog.stages for i in sp.instructions)
+    assert sorted((e["stage"], e["op"], e["label"]) for e in doc["events"]) == want
+    gantt = json.loads((tmp_path / "gantt.json").read_text())
+    assert set(gantt) == {"0", "1"} and gantt["0"] and gantt["1"]
