@@ -1951,9 +1951,20 @@ def execute(plan, program: Optional[Program] = None, *, schedule: str = GPIPE, s
     "oom" naming the device, stage and instruction; a step that does not finish
     within `timeout` seconds raises kind "deadlock" naming the instruction the
     stage is blocked on."""
-    if device_memory is not None and enforce_memory and torch.cuda.is_available():
+    capped = device_memory is not None and enforce_memory and torch.cuda.is_available()
+    if capped:
         total = torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory
         torch.cuda.set_per_process_memory_fraction(min(1.0, device_memory / total))
+    try:
+        return _execute(plan, program, schedule, steps, params, inputs, seed, adam, record,
+                        collect, update, timeout)
+    finally:
+        if capped:
+            torch.cuda.set_per_process_memory_fraction(1.0)
+
+
+def _execute(plan, program, schedule, steps, params, inputs, seed, adam, record, collect, update,
+             timeout) -> ExecResult:
     ex = Executor(plan, program, schedule=schedule, params=params, inputs=inputs, seed=seed,
                   adam=adam)
     ex.runner.keep_outputs = collect
