@@ -72,6 +72,7 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int NACC = 2;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -315,8 +316,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tc_commit(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (Cfg::NACC == 2) {
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        } else {
+          acc_phase ^= 1;
+        }
       }
     }
   } else {
@@ -368,13 +373,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 // rows into its own TMEM.  Per-CTA smem traffic per MMA drops to (4 + BN/32) KB
 // per 128*BN/256 cycles, and the 256-row tiles halve the wave count for the
 // N = 2048 projections of the GPT plans.
+// BN = 512: 256 x 512 pair tiles, two N = 256 MMAs per k-step into all 512 TMEM
+// columns (one accumulator, so the epilogue of a tile is not overlapped with the next
+// tile's MMAs) -- 25% fewer operand bytes per MAC than 256 x 256, for the wide GEMMs
+// whose per-clock rate the L2 -> SM operand stream sets.
 template <int BN>
 struct Gemm2Cfg {
   static constexpr int A_BYTES = BM * BK * 2;            // 128 rows of A
   static constexpr int B_BYTES = (BN / 2) * BK * 2;      // half of the B columns
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 6 : 8;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int STAGES = (BN == 512) ? 4 : ((BN == 256) ? 6 : 8);
+  static constexpr int NACC = (BN == 512) ? 1 : 2;       // TMEM accumulator buffers
+  static constexpr int TMEM_COLS = NACC * BN;
   static constexpr int EPI_STAGE = kEpiWarps * 32 * 16 * 4;   // 32 rows x 16 fp32 per warp
   // [stages][epi staging][C store staging][barriers]; both staging areas 1024B aligned
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2 * EPI_STAGE + 512;
@@ -634,7 +644,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           } else {
             tma_load_4d_2sm(&tmA, fb, a_dst, k0, m0, b1, b0);
           }
-          if (p.b_mn5) {
+          if (BN == 512) {
+            // two N = 256 halves; this CTA stages 128 columns of each
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int nh = tl.n0 + h * 256 + rank * 128;
+              uint8_t* bh = b_dst + h * (128 * BK * 2);
+              if (p.b_mn5) {
+                tma_load_5d_2sm(&tmB, fb, bh, 0, k0, nh / 64, b1, b0);
+              } else if (p.b_mn) {
+                for (int i = 0; i < 2; ++i)
+                  tma_load_4d_2sm(&tmB, fb, bh + i * 8192, nh + 64 * i, k0, b1, b0);
+              } else {
+                tma_load_4d_2sm(&tmB, fb, bh, k0, nh, b1, b0);
+              }
+            }
+          } else if (p.b_mn5) {
             tma_load_5d_2sm(tl.narrow ? &tmBn : &tmB, fb, b_dst, 0, k0, n0 / 64, b1, b0);
           } else if (p.b_mn) {
             for (int i = 0; i < nw / 64; ++i)
@@ -651,7 +676,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      const uint32_t idesc_w = umma_idesc_bf16(2 * BM, BN, p.a_mn, p.b_mn);
+      const uint32_t idesc_w = umma_idesc_bf16(2 * BM, BN == 512 ? 256 : BN, p.a_mn, p.b_mn);
       const uint32_t idesc_n = umma_idesc_bf16(2 * BM, BN / 2, p.a_mn, p.b_mn);
       const uint32_t a_lbo = p.a_mn ? 8192u : 16u, b_lbo = p.b_mn ? 8192u : 16u;
       const uint32_t a_kstep = p.a_mn ? 2048u : 32u, b_kstep = p.b_mn ? 2048u : 32u;
@@ -672,8 +697,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = umma_desc_sw128(a_base + kk * a_kstep, a_lbo, 1024u);
-            const uint64_t bd = umma_desc_sw128(b_base + kk * b_kstep, b_lbo, 1024u);
-            tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            if (BN == 512) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint64_t bd =
+                    umma_desc_sw128(b_base + h * (128 * BK * 2) + kk * b_kstep, b_lbo, 1024u);
+                tc_mma_f16_2sm(d_tmem + h * 256, ad, bd, idesc, (kb | kk) != 0);
+              }
+            } else {
+              const uint64_t bd = umma_desc_sw128(b_base + kk * b_kstep, b_lbo, 1024u);
+              tc_mma_f16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            }
           }
           tc_commit_2sm_mc(&empty[stage]);
           if (++stage == STAGES) {
@@ -682,8 +716,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         tc_commit_2sm_mc(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (Cfg::NACC == 2) {
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        } else {
+          acc_phase ^= 1;
+        }
       }
     }
   } else {
@@ -786,8 +824,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (Cfg::NACC == 2) {
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      } else {
+        acc_phase ^= 1;
+      }
     }
     if ((p.c_red || p.c_tma) && lane == 0) bulk_wait_all_g();   // staging reads + C writes done
   }
@@ -991,6 +1033,7 @@ static int launch_gemm_2sm(const CUtensorMap& ma, const CUtensorMap& mb, const C
   const int r = wide % pairs;
   p.n_wide = wide;
   if (!no_split && BN == 256 && wide > pairs && r > 0 && 2 * r <= pairs) p.n_wide = wide - r;
+  // (BN = 512 has no half-width tail tiles: it is only chosen when its waves are full)
   p.num_tiles = p.n_wide + 2 * (wide - p.n_wide);
   if (p.num_tiles < pairs) pairs = p.num_tiles;
   gemm_bf16_2sm_kernel<BN><<<2 * pairs, kThreads, Cfg::SMEM, stream>>>(ma, mb, mbn, mc, mx, p);
@@ -1009,7 +1052,7 @@ static inline int preload_one(F* f) {
 int preload_gemm() {
   return preload_one(gemm_bf16_kernel<64>) | preload_one(gemm_bf16_kernel<128>) |
          preload_one(gemm_bf16_kernel<256>) | preload_one(gemm_bf16_2sm_kernel<128>) |
-         preload_one(gemm_bf16_2sm_kernel<256>);
+         preload_one(gemm_bf16_2sm_kernel<256>) | preload_one(gemm_bf16_2sm_kernel<512>);
 }
 }  // namespace mp
 
@@ -1107,10 +1150,19 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
   (void)nb;
   if (two_sm) {
     BN = mode == 128 ? 128 : 256;
+    // 256 x 512 pair tiles on the wide GEMMs when their waves come out (nearly) full
+    static const bool bn512 = getenv("MPEXEC_GEMM_BN512") != nullptr &&
+                              atoi(getenv("MPEXEC_GEMM_BN512")) != 0;
+    if (bn512 && mode != 128 && N % 512 == 0) {
+      const int64_t t512 = ((M + 255) / 256) * (N / 512) * nbatch0 * nbatch1;
+      const int64_t pairs_n = num_sms() / 2;
+      const int64_t waves = (t512 + pairs_n - 1) / pairs_n;
+      if (waves >= 4 && t512 * 100 >= waves * pairs_n * 95) BN = 512;
+    }
   } else {
     BN = (N > 128) ? 256 : (N > 64 ? 128 : 64);
   }
-  const int b_box_n = two_sm ? BN / 2 : BN;
+  const int b_box_n = two_sm ? (BN == 512 ? 128 : BN / 2) : BN;
   CUtensorMap mbn;
   if (bd[3] == 1) {
     p.b_mn = 1;
@@ -1187,8 +1239,9 @@ extern "C" int mp_gemm_bf16_ex(const void* A, const int64_t* ad, const void* B,
   static const bool no_aux_db = getenv("MPEXEC_GEMM_NO_AUX_DB") != nullptr;
   p.aux_db = (p.aux_tma && !p.c_tma && !no_aux_db) ? 1 : 0;
   if (two_sm)
-    rc = (BN == 256) ? launch_gemm_2sm<256>(ma, mb, mbn, mc, mx, p, s)
-                     : launch_gemm_2sm<128>(ma, mb, mbn, mc, mx, p, s);
+    rc = (BN == 512) ? launch_gemm_2sm<512>(ma, mb, mbn, mc, mx, p, s)
+         : (BN == 256) ? launch_gemm_2sm<256>(ma, mb, mbn, mc, mx, p, s)
+                       : launch_gemm_2sm<128>(ma, mb, mbn, mc, mx, p, s);
   else if (BN == 256)
     rc = launch_gemm<256>(ma, mb, p, s);
   else if (BN == 128)

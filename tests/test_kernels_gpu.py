@@ -393,3 +393,50 @@ def test_pack_unpack_box_rows(shape, lo, ext):
     assert torch.equal(dst[sl], t[sl])
     dst[sl] = 0
     assert not dst.any()
+
+
+def test_gemm_bn512_pair_tiles():
+    """256 x 512 pair tiles (MPEXEC_GEMM_BN512=1, one TMEM accumulator, two N = 256
+    MMAs per k-step) on the wide GPT shapes, every B layout and the fused epilogues,
+    against torch fp32 (run in a subprocess: the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = textwrap.dedent("""
+        import torch
+        from paper_2201_12023_b200 import native
+        def rel(x, r):
+            return float((x.float() - r).norm() / r.norm())
+        torch.manual_seed(0)
+        M, N, K = 8192, 8192, 512
+        a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        for tb in (0, 1):
+            b = (torch.randn(N, K, device="cuda").to(torch.bfloat16).t() if tb else
+                 torch.randn(K, N, device="cuda").to(torch.bfloat16)) * 0.1
+            acc = a.float() @ b.float()
+            out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            native.gemm(a, b, out)
+            assert rel(out, acc) < 1e-2, ("plain", tb)
+            act = torch.empty_like(out)
+            native.gemm(a, b, out, epilogue=native.EPI_GELU_DUAL, aux=act)
+            assert rel(out, acc) < 1e-2 and rel(act, torch.nn.functional.gelu(acc, approximate="tanh")) < 1e-2
+            aux = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+            native.gemm(a, b, out, epilogue=native.EPI_ADD, aux=aux)
+            assert rel(out, acc + aux.float()) < 1e-2
+            native.gemm(a, b, out, epilogue=native.EPI_GELU_GRAD, aux=aux)
+            xf = aux.float().requires_grad_()
+            torch.nn.functional.gelu(xf, approximate="tanh").backward(acc)
+            assert rel(out, xf.grad) < 1e-2
+            c = torch.randn(M, N, device="cuda")
+            ref = c + acc
+            native.gemm(a, b, c, beta=1.0)
+            assert rel(c, ref) < 2e-3
+        print("ok")
+    """)
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                         cwd=root, env={**os.environ, "PYTHONPATH": str(root),
+                                        "MPEXEC_GEMM_BN512": "1"})
+    assert res.returncode == 0 and "ok" in res.stdout, res.stdout[-2000:] + res.stderr[-3000:]
