@@ -160,7 +160,7 @@ struct FaFwdParams {
 // smem: Q 16K | K[2] 32K | V 16K | P 32K | barriers  (97 KB: two CTAs per SM).
 // With P in TMEM (PT, the default) the P tiles are not allocated: 65 KB.
 constexpr int FA_FWD_SMEM = FA_TILE * 6 + 1024 + 256;
-constexpr int FA_FWD_SMEM_PT = FA_TILE * 4 + 1024 + 256;
+constexpr int FA_FWD_SMEM_PT = FA_TILE * 5 + 1024 + 256;   // PT: V double-buffered
 
 // tcgen05.mma with A read from tensor memory (TS form): P V with P in TMEM
 __device__ __forceinline__ void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
@@ -190,14 +190,17 @@ __global__ void __launch_bounds__(192, 2)
                                              ~(uintptr_t)1023);
   uint8_t* sQ = smem;
   uint8_t* sK = smem + FA_TILE;          // 2 stages
-  uint8_t* sV = smem + 3 * FA_TILE;      // 1 stage
+  uint8_t* sV = smem + 3 * FA_TILE;      // 1 stage (PT: 2, in the smem freed by P)
   uint8_t* sP = smem + 4 * FA_TILE;      // 2 chunks of 64 keys (not PT)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (PT ? 4 : 6) * FA_TILE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (PT ? 5 : 6) * FA_TILE);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;    // [2]
   uint64_t* k_empty = bars + 3;   // [2]
-  uint64_t* v_full = bars + 5;
-  uint64_t* v_empty = bars + 6;
+  uint64_t* v_full = bars + 5;    // [PT: 2] stage 1 at bars + 16
+  uint64_t* v_empty = bars + 6;   // [PT: 2] stage 1 at bars + 17
+  constexpr int VST = PT ? 2 : 1;
+  auto vfull = [&](int st) { return st ? bars + 16 : v_full; };
+  auto vempty = [&](int st) { return st ? bars + 17 : v_empty; };
   uint64_t* s_full = bars + 7;
   uint64_t* s_free = bars + 8;
   uint64_t* p_full = bars + 9;     // P keys 0-63 in smem (4 softmax warps)
@@ -223,8 +226,10 @@ __global__ void __launch_bounds__(192, 2)
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
     }
-    mbar_init(v_full, 1);
-    mbar_init(v_empty, 1);
+    for (int i = 0; i < VST; ++i) {
+      mbar_init(vfull(i), 1);
+      mbar_init(vempty(i), 1);
+    }
     mbar_init(s_full, 1);
     mbar_init(s_free, 4);
     mbar_init(p_full, 4);
@@ -249,9 +254,11 @@ __global__ void __launch_bounds__(192, 2)
         mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[st], FA_TILE);
         tma_load_2d(&tmK, &k_full[st], sK + st * FA_TILE, hh * FA_D, krow0 + j * FA_BN);
-        mbar_wait(v_empty, (j & 1) ^ 1);
-        mbar_arrive_expect_tx(v_full, FA_TILE);
-        tma_load_2d(&tmV, v_full, sV, hh * FA_D, krow0 + j * FA_BN);
+        const int vs = VST == 2 ? (j & 1) : 0;
+        const uint32_t vpar = VST == 2 ? (((j >> 1) & 1) ^ 1) : ((j & 1) ^ 1);
+        mbar_wait(vempty(vs), vpar);
+        mbar_arrive_expect_tx(vfull(vs), FA_TILE);
+        tma_load_2d(&tmV, vfull(vs), sV + vs * FA_TILE, hh * FA_D, krow0 + j * FA_BN);
       }
     }
   } else if (warp == 1) {
@@ -276,7 +283,9 @@ __global__ void __launch_bounds__(192, 2)
       issue_s(0);
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) issue_s(j + 1);
-        mbar_wait(v_full, j & 1);
+        const int vs = VST == 2 ? (j & 1) : 0;
+        mbar_wait(vfull(vs), VST == 2 ? ((j >> 1) & 1) : (j & 1));
+        const uint32_t vb = v_base + vs * FA_TILE;
         // O += P V in two halves of 64 keys: the first half starts as soon as the
         // softmax warps have written P's first 64 keys, and its completion
         // (p0_free) lets them write the next tile's first half while the
@@ -288,7 +297,7 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int kk = h * 4 + k4;
-            const uint64_t bd = umma_desc_sw128(v_base + kk * 2048, 8192, 1024);
+            const uint64_t bd = umma_desc_sw128(vb + kk * 2048, 8192, 1024);
             if (PT) {
               tc_mma_f16_ts(tO, tP + kk * 8, bd, id_o, (j | kk) != 0);   // 16 keys = 8 columns
             } else {
@@ -298,7 +307,7 @@ __global__ void __launch_bounds__(192, 2)
           }
           if (h == 0) tc_commit(p0_free);
         }
-        tc_commit(v_empty);
+        tc_commit(vempty(vs));
         tc_commit(o_done);
       }
     }
