@@ -10,7 +10,7 @@
 // (tokens, hidden) tensors of the projection matmuls, so head split / merge
 // stay views.  d = 64 (GPT-1.3B), s % 128 == 0.
 //
-// Forward (one CTA per 128-query tile of one (b, head)):
+// Forward (persistent: work tiles of 128 queries of one (b, head)):
 //   warp 0     TMA: Q once, K/V tiles through a 2-stage ring
 //   warp 1     tcgen05.mma: S = Q K^T (TMEM, 128 cols), O += P V (TMEM, 64 cols)
 //   warps 2-5  softmax, one thread per query row: online max / sum in the log2
@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <cstring>
 #include "common.cuh"
 #include "../../include/mp_exec.h"
 
@@ -452,6 +453,293 @@ __global__ void __launch_bounds__(192, 2)
     }
     // natural-log LSE of the scaled scores: ln(l) + m_used * ln 2
     p.lse[(int64_t)bh * p.s + qt * FA_BM + r] = logf(l) + m_used * 0.6931471805599453f;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+// Persistent forward (P in TMEM): two CTAs per SM walk work tiles w = (bh, query
+// tile) with stride gridDim.x.  Barrier phases run on the CTA-global key-tile
+// counter J, so the pipeline does not drain between work tiles: Q is
+// double-buffered (the next tile's Q lands while this one still streams K/V),
+// the next tile's first S = Q K^T is issued as soon as the last S of this tile
+// has been read, and the O epilogue (TMEM -> bf16 global) overlaps that S MMA;
+// the next tile's first P V (which overwrites O) waits for o_free.
+// smem: Q[2] 32K | K[2] 32K | V[2] 32K | barriers (97 KB: two CTAs per SM).
+constexpr int FA_FWD_SMEM_PERSIST = FA_TILE * 6 + 1024 + 256;
+
+__global__ void __launch_bounds__(192, 2)
+    fa_fwd_persist_kernel(const __grid_constant__ CUtensorMap tmQ,
+                          const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV, const FaFwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sQ = smem;                    // 2 stages
+  uint8_t* sK = smem + 2 * FA_TILE;      // 2 stages
+  uint8_t* sV = smem + 4 * FA_TILE;      // 2 stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * FA_TILE);
+  uint64_t* q_full = bars;         // [2]
+  uint64_t* q_empty = bars + 2;    // [2]
+  uint64_t* k_full = bars + 4;     // [2]
+  uint64_t* k_empty = bars + 6;    // [2]
+  uint64_t* v_full = bars + 8;     // [2]
+  uint64_t* v_empty = bars + 10;   // [2]
+  uint64_t* s_full = bars + 12;
+  uint64_t* s_free = bars + 13;
+  uint64_t* p_full = bars + 14;    // P keys 0-63 in TMEM
+  uint64_t* p_full1 = bars + 15;   // P keys 64-127
+  uint64_t* p0_free = bars + 16;   // P V has read P keys 0-63
+  uint64_t* o_done = bars + 17;
+  uint64_t* o_free = bars + 18;    // epilogue has read O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qt = p.s / FA_BM;
+  const int n_work = n_qt * p.B * p.H;
+  const int n_kv = p.nkv;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 4);
+    mbar_init(p_full, 4);
+    mbar_init(p_full1, 4);
+    mbar_init(p0_free, 1);
+    mbar_init(o_done, 1);
+    mbar_init(o_free, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tO = tmem + 128, tP = tmem + 192;
+
+  // work tile -> (first row of the sequence, head, query tile); consecutive w share
+  // a (b, head) so co-resident CTAs re-read the same K/V from L2
+  auto decode = [&](int w, int& row0, int& hh, int& qt, int& bh) {
+    bh = w / n_qt;
+    qt = w - bh * n_qt;
+    const int b = bh / p.H;
+    hh = bh - b * p.H;
+    row0 = b * p.s;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int J = 0, tt = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++tt) {
+        int row0, hh, qt, bh;
+        decode(w, row0, hh, qt, bh);
+        const int qs = tt & 1;
+        mbar_wait(&q_empty[qs], ((tt >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qs], FA_TILE);
+        tma_load_2d(&tmQ, &q_full[qs], sQ + qs * FA_TILE, hh * FA_D, row0 + qt * FA_BM);
+        const int krow0 = row0 + p.kv0;
+        for (int j = 0; j < n_kv; ++j, ++J) {
+          const int st = J & 1;
+          const uint32_t par = ((J >> 1) & 1) ^ 1;
+          mbar_wait(&k_empty[st], par);
+          mbar_arrive_expect_tx(&k_full[st], FA_TILE);
+          tma_load_2d(&tmK, &k_full[st], sK + st * FA_TILE, hh * FA_D, krow0 + j * FA_BN);
+          mbar_wait(&v_empty[st], par);
+          mbar_arrive_expect_tx(&v_full[st], FA_TILE);
+          tma_load_2d(&tmV, &v_full[st], sV + st * FA_TILE, hh * FA_D, krow0 + j * FA_BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = umma_idesc_bf16(128, 128, 0, 0);   // Q K-major, K K-major
+      const uint32_t id_o = umma_idesc_bf16(128, 64, 0, 1);    // P (TMEM), V MN-major
+      const uint32_t v_base = smem_u32(sV);
+      const int n_tiles = blockIdx.x < n_work ? (n_work - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      // S for global key tile Jn, which is key tile jn of local work tile tn
+      auto issue_s = [&](int Jn, int tn, int jn) {
+        const int qs = tn & 1;
+        if (jn == 0) mbar_wait(&q_full[qs], (tn >> 1) & 1);
+        const int st = Jn & 1;
+        mbar_wait(&k_full[st], (Jn >> 1) & 1);
+        if (Jn > 0) mbar_wait(s_free, (Jn - 1) & 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ + qs * FA_TILE);
+        const uint32_t k_base = smem_u32(sK + st * FA_TILE);
+#pragma unroll
+        for (int kk = 0; kk < FA_D / 16; ++kk)
+          tc_mma_f16(tS, umma_desc_sw128(q_base + kk * 32, 16, 1024),
+                     umma_desc_sw128(k_base + kk * 32, 16, 1024), id_s, kk > 0);
+        tc_commit(s_full);
+        tc_commit(&k_empty[st]);
+        if (jn == n_kv - 1) tc_commit(&q_empty[qs]);
+      };
+      if (n_tiles > 0) issue_s(0, 0, 0);
+      int J = 0;
+      for (int tt = 0; tt < n_tiles; ++tt) {
+        for (int j = 0; j < n_kv; ++j, ++J) {
+          if (j + 1 < n_kv)
+            issue_s(J + 1, tt, j + 1);
+          else if (tt + 1 < n_tiles)
+            issue_s(J + 1, tt + 1, 0);
+          // the first P V of a tile overwrites O: the previous epilogue must have read it
+          if (j == 0 && tt > 0) mbar_wait(o_free, (tt - 1) & 1);
+          const int st = J & 1;
+          mbar_wait(&v_full[st], (J >> 1) & 1);
+          const uint32_t vb = v_base + st * FA_TILE;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait(h ? p_full1 : p_full, J & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int kk = h * 4 + k4;
+              tc_mma_f16_ts(tO, tP + kk * 8, umma_desc_sw128(vb + kk * 2048, 8192, 1024), id_o,
+                            (j | kk) != 0);
+            }
+            if (h == 0) tc_commit(p0_free);
+          }
+          tc_commit(&v_empty[st]);
+          tc_commit(o_done);
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;                       // query row within the tile
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    int J = 0;
+    for (int w = blockIdx.x, tt = 0; w < n_work; w += gridDim.x, ++tt) {
+      int row0, hh, qt, bh;
+      decode(w, row0, hh, qt, bh);
+      float m_used = -INFINITY;                        // log2-domain running max
+      float l = 0.f;
+      for (int j = 0; j < n_kv; ++j, ++J) {
+        mbar_wait(s_full, J & 1);
+        tc_fence_after();
+        uint32_t sv[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + lane_off + c * 32, sv[c]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int e = 0; e < 32; e += 2)
+            mx = fmax3(mx, __uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1]));
+        mx *= p.scale_log2;
+        const bool need = (mx > m_used + 8.f);
+        float alpha = 1.f;
+        if (need) {
+          alpha = (m_used == -INFINITY) ? 0.f : ex2(m_used - mx);
+          m_used = mx;
+        }
+        // P (TMEM) must not be overwritten before the previous P V has read it; at
+        // j == 0 the previous tile's epilogue already waited for its last P V
+        const bool any_need = __any_sync(0xffffffffu, need);
+        if (j > 0) {
+          mbar_wait(any_need ? o_done : p0_free, (J - 1) & 1);
+          tc_fence_after();
+          if (any_need) {
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o16[16];
+              tmem_ld16(tO + lane_off + c * 16, o16);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                o16[e] = __float_as_uint(__uint_as_float(o16[e]) * alpha);
+              tmem_st16(tO + lane_off + c * 16, o16);
+            }
+            tmem_st_wait();
+          }
+        }
+        l *= alpha;
+        const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2), nm2 = f2pack(-m_used, -m_used);
+        uint64_t sum2 = f2pack(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c == 2) {
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+            if (j > 0 && !any_need) {
+              mbar_wait(o_done, (J - 1) & 1);
+              tc_fence_after();
+            }
+          }
+          const uint32_t(&t32)[32] = sv[c];
+          uint32_t pk[16];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            float pv[8];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              float x0, x1;
+              f2unpack(ffma2(f2pack(__uint_as_float(t32[t * 8 + e]),
+                                    __uint_as_float(t32[t * 8 + e + 1])), sc2, nm2), x0, x1);
+              pv[e] = ex2(x0);
+              pv[e + 1] = ex2(x1);
+              sum2 = fadd2(sum2, f2pack(pv[e], pv[e + 1]));
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pk[t * 4 + e] = pack_bf2(pv[2 * e], pv[2 * e + 1]);
+          }
+          tmem_st16(tP + lane_off + c * 16, pk);
+        }
+        float s0, s1;
+        f2unpack(sum2, s0, s1);
+        l += s0 + s1;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full1);
+      }
+      // epilogue: O / l -> bf16, then release O for the next tile's first P V
+      mbar_wait(o_done, (J - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      uint16_t* orow = p.O + (int64_t)(row0 + qt * FA_BM + r) * p.ld + hh * FA_D;
+      uint32_t o16[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tO + lane_off + c * 16, o16[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_free);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+        uint32_t pk[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          pk[e] = pack_bf2(__uint_as_float(o16[c][2 * e]) * inv,
+                           __uint_as_float(o16[c][2 * e + 1]) * inv);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      p.lse[(int64_t)bh * p.s + qt * FA_BM + r] = logf(l) + m_used * 0.6931471805599453f;
+    }
   }
 
   tc_fence_before();
@@ -1043,6 +1331,7 @@ static inline int preload_one(F* f) {
 }
 int preload_attention() {
   return preload_one(fa_fwd_kernel<true>) | preload_one(fa_fwd_kernel<false>) |
+         preload_one(fa_fwd_persist_kernel) |
          preload_one(fa_bwd_kernel<true>) | preload_one(fa_bwd_kernel<false>) | preload_one(fa_bwd_pre_kernel) |
          preload_one(attn_combine_scale_kernel) | preload_one(attn_combine_finish_kernel);
 }
@@ -1073,25 +1362,40 @@ extern "C" int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void*
   if ((rc = fa_map(&mq, q, B * s, ld)) || (rc = fa_map(&mk, k, B * s, ld)) ||
       (rc = fa_map(&mv, v, B * s, ld)))
     return rc;
-  // MPEXEC_FA_FWD_SMEM_P=1: P through shared memory (SS-form P V), for A/B runs.
+  // MPEXEC_FA_FWD=tile: one CTA per query tile (P in TMEM); =smem: the same with P
+  // through shared memory (SS-form P V).  Default: the persistent kernel.
   // P in TMEM measured 127.9 -> 121.6 us at B=8, H=32, s=1024 (bench_gemm.py --attn)
-  static const bool smem_p = getenv("MPEXEC_FA_FWD_SMEM_P") != nullptr;
+  static const int mode = [] {
+    const char* e = getenv("MPEXEC_FA_FWD");
+    if (e && !strcmp(e, "smem")) return 2;
+    if (e && !strcmp(e, "tile")) return 1;
+    return 0;
+  }();
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(fa_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FA_FWD_SMEM);
     cudaFuncSetAttribute(fa_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FA_FWD_SMEM_PT);
+    cudaFuncSetAttribute(fa_fwd_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_FWD_SMEM_PERSIST);
     configured = true;
   }
   FaFwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, (int)(kv_len / FA_BN),
                 scale * 1.4426950408889634f, reinterpret_cast<uint16_t*>(o), lse};
-  dim3 grid((unsigned)(s / FA_BM), (unsigned)(B * H));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (smem_p)
-    fa_fwd_kernel<false><<<grid, 192, FA_FWD_SMEM, st>>>(mq, mk, mv, p);
-  else
-    fa_fwd_kernel<true><<<grid, 192, FA_FWD_SMEM_PT, st>>>(mq, mk, mv, p);
+  if (mode == 0) {
+    const int64_t work = (s / FA_BM) * B * H;
+    const int64_t slots = 2 * (int64_t)num_sms();
+    fa_fwd_persist_kernel<<<(unsigned)(work < slots ? work : slots), 192, FA_FWD_SMEM_PERSIST,
+                            st>>>(mq, mk, mv, p);
+  } else {
+    dim3 grid((unsigned)(s / FA_BM), (unsigned)(B * H));
+    if (mode == 2)
+      fa_fwd_kernel<false><<<grid, 192, FA_FWD_SMEM, st>>>(mq, mk, mv, p);
+    else
+      fa_fwd_kernel<true><<<grid, 192, FA_FWD_SMEM_PT, st>>>(mq, mk, mv, p);
+  }
   MP_CHECK_LAUNCH();
   return 0;
 }
