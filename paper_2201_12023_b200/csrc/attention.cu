@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include "common.cuh"
@@ -762,6 +763,7 @@ struct FaBwdParams {
   float* dQacc;       // fp32 (T, ld), zero-initialised
   uint16_t* dK;
   uint16_t* dV;
+  long long* trace;   // diagnostics (MPEXEC_FA_BWD_TRACE): globaltimer per query tile
 };
 
 // smem: K 16K | V 16K | Q[2] 32K | dO[2] 32K | P^T[2] 64K | dS^T[2] 64K | barriers (224 KB)
@@ -783,6 +785,18 @@ constexpr int FA_BWD_THREADS = 448;   // TMA, MMA, 8 P/dS warps, 4 dQ warps
 // form), so P^T costs neither shared-memory stores nor shared-memory operand reads
 // (the backward is bound by shared-memory bandwidth); the dQ accumulator is
 // single-buffered to make room for it.
+// diagnostics: %globaltimer stamp `k` of query tile g.  Compiled in only with
+// -DMP_FA_TRACE (MPEXEC_NVCC_EXTRA) and written when MPEXEC_FA_BWD_TRACE names a file
+__device__ __forceinline__ void fa_stamp(long long* trace, int g, int k) {
+#ifdef MP_FA_TRACE
+  if (trace && g < 1024) {
+    long long ts;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ts));
+    trace[((int64_t)blockIdx.x * 1024 + g) * 8 + k] = ts;
+  }
+#endif
+}
+
 template <bool PT>
 __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -898,8 +912,9 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
             tma_load_2d(&tmV, kv_full, sV, hh * FA_D, row0 + p.kv0 + kt * FA_BN);
           }
         }
+        const int wn = w + (int)gridDim.x;
         if (i + 1 < n_q) fetch(w, i + 1);
-        else if (w + (int)gridDim.x < n_work) fetch(w + gridDim.x, 0);
+        else if (wn < n_work) fetch(wn, 0);
       }
     }
   } else if (warp == 1) {
@@ -915,6 +930,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
           mbar_wait(acc_free, (t - 1) & 1);
           tc_fence_after();
         }
+        fa_stamp(p.trace, gj, 5);
         const uint32_t pt = smem_u32(sPt + bj * 2 * FA_TILE), ds = smem_u32(sdSt + bj * 2 * FA_TILE);
         const uint32_t qb = smem_u32(sQ + bj * FA_TILE), dob = smem_u32(sdO + bj * FA_TILE);
         if (PT) {
@@ -948,6 +964,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         } else if (gj >= 2) {
           mbar_wait(&dq_free[bj], ((gj >> 1) & 1) ^ 1);
         }
+        fa_stamp(p.trace, gj, 6);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < FA_BN / 16; ++kk)
@@ -962,6 +979,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
           const int st = g & 1;
           mbar_wait(&q_full[st], (g >> 1) & 1);
           if (g > 0) mbar_wait(s_free, (g - 1) & 1);    // S^T/dP^T(g-1) in the P warps' registers
+          fa_stamp(p.trace, g, 4);
           tc_fence_after();
           const uint32_t q_base = smem_u32(sQ + st * FA_TILE);
           const uint32_t do_base = smem_u32(sdO + st * FA_TILE);
@@ -1000,11 +1018,14 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       for (int i = 0; i < n_q; ++i, ++g) {
         const int bi = g & 1;
         mbar_wait(&q_full[bi], (g >> 1) & 1);   // lse / D of g staged
+        if (warp == 2 && lane == 0) fa_stamp(p.trace, g, 0);
         mbar_wait(st_full, g & 1);
+        if (warp == 2 && lane == 0) fa_stamp(p.trace, g, 1);
         tc_fence_after();
         // this P^T / dS^T buffer was last read by the MMAs of g-2
         // (PT: dQ is staged elsewhere, so the dK / dQ MMAs of g-2 are the last readers)
         if (g >= 2) mbar_wait(PT ? &dq_full[bi] : &pbuf_free[bi], ((g >> 1) & 1) ^ 1);
+        if (warp == 2 && lane == 0) fa_stamp(p.trace, g, 2);
         uint8_t* pt = sPt + bi * 2 * FA_TILE;
         uint8_t* dst = sdSt + bi * 2 * FA_TILE;
 
@@ -1086,6 +1107,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ps_full);
+        if (warp == 2 && lane == 0) fa_stamp(p.trace, g, 3);
       }
       // dK (half 0) / dV (half 1) epilogue: key row r
       const int bh = w / p.n_kt, kt = w - (w / p.n_kt) * p.n_kt;
@@ -1132,6 +1154,7 @@ __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
       for (int i = 0; i < n_q; ++i, ++g) {
         const int bj = g & 1;
         mbar_wait(&dq_full[bj], (g >> 1) & 1);
+        if (leader) fa_stamp(p.trace, g, 7);
         tc_fence_after();
         uint32_t t16[4][16];
 #pragma unroll
@@ -1440,9 +1463,19 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
     configured = true;
   }
   FaBwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, (int)(kv_len / FA_BN), scale, lse,
-                dvec, dq_acc, reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv)};
+                dvec, dq_acc, reinterpret_cast<uint16_t*>(dk), reinterpret_cast<uint16_t*>(dv),
+                nullptr};
   const int64_t work = (kv_len / FA_BN) * B * H;
   dim3 grid((unsigned)(work < num_sms() ? work : num_sms()));
+  // MPEXEC_FA_BWD_TRACE=<file>: diagnostics only -- every launch syncs and overwrites
+  // <file> with int64 globaltimer stamps [grid][1024][8] (fa_stamp slots, -1 unused)
+  static const char* trace_path = getenv("MPEXEC_FA_BWD_TRACE");
+  static long long* trace_buf = nullptr;
+  if (trace_path) {
+    if (!trace_buf) cudaMalloc(&trace_buf, (size_t)num_sms() * 1024 * 8 * sizeof(long long));
+    cudaMemsetAsync(trace_buf, 0xff, (size_t)num_sms() * 1024 * 8 * sizeof(long long), st);
+    p.trace = trace_buf;
+  }
   // MPEXEC_FA_BWD_PT=1: P^T in TMEM (TS-form dV MMA, single dQ buffer).  Parity-green
   // but measured no faster (273.0 -> 275.1 us): off by default
   static const bool smem_p = getenv("MPEXEC_FA_BWD_PT") == nullptr;
@@ -1451,6 +1484,17 @@ extern "C" int mp_attn_bwd_kv(const void* q, const void* k, const void* v, const
   else
     fa_bwd_kernel<true><<<grid, FA_BWD_THREADS, FA_BWD_SMEM, st>>>(mq, mk, mv, mdo, mdq, p);
   MP_CHECK_LAUNCH();
+  if (trace_path) {
+    const size_t n = (size_t)grid.x * 1024 * 8;
+    long long* h = (long long*)malloc(n * sizeof(long long));
+    cudaMemcpyAsync(h, trace_buf, n * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE* fp = fopen(trace_path, "wb")) {
+      fwrite(h, sizeof(long long), n, fp);
+      fclose(fp);
+    }
+    free(h);
+  }
   return 0;
 }
 
