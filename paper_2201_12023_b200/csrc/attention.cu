@@ -475,6 +475,27 @@ __global__ void __launch_bounds__(192, 2)
 // smem: Q[2] 32K | K[2] 32K | V[2] 32K | barriers (97 KB: two CTAs per SM).
 constexpr int FA_FWD_SMEM_PERSIST = FA_TILE * 6 + 1024 + 256;
 
+// 2^x for a pair on the FMA / ALU pipes instead of MUFU (which runs at 16 / clk / SM and
+// bounds the forward at d = 64): x = n + f with n = rint(x) via the 1.5 * 2^23 trick,
+// 2^f on [-0.5, 0.5] by a degree-3 fit (max relative error 7.8e-5, far below bf16's
+// 3.9e-3), and n added straight into the exponent field.  x >= -126 keeps the exponent
+// field non-negative (2^-126 is 0 for the softmax either way).
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& y0, float& y1) {
+  const uint64_t x = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t t = fadd2(x, f2pack(12582912.f, 12582912.f));
+  const uint64_t fr = ffma2(fadd2(t, f2pack(-12582912.f, -12582912.f)), f2pack(-1.f, -1.f), x);
+  uint64_t pp = ffma2(f2pack(0.055268411f, 0.055268411f), fr, f2pack(0.24262036f, 0.24262036f));
+  pp = ffma2(pp, fr, f2pack(0.69324332f, 0.69324332f));
+  pp = ffma2(pp, fr, f2pack(0.99992698f, 0.99992698f));
+  float p0, p1, t0, t1;
+  f2unpack(pp, p0, p1);
+  f2unpack(t, t0, t1);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
+// EMU: how many of every eight exponent pairs go to exp2_poly2 instead of MUFU
+template <int EMU>
 __global__ void __launch_bounds__(192, 2)
     fa_fwd_persist_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -699,8 +720,12 @@ __global__ void __launch_bounds__(192, 2)
               float x0, x1;
               f2unpack(ffma2(f2pack(__uint_as_float(t32[t * 8 + e]),
                                     __uint_as_float(t32[t * 8 + e + 1])), sc2, nm2), x0, x1);
-              pv[e] = ex2(x0);
-              pv[e + 1] = ex2(x1);
+              if (((t * 4 + e / 2) & 7) < EMU) {
+                exp2_poly2(x0, x1, pv[e], pv[e + 1]);
+              } else {
+                pv[e] = ex2(x0);
+                pv[e + 1] = ex2(x1);
+              }
               sum2 = fadd2(sum2, f2pack(pv[e], pv[e + 1]));
             }
 #pragma unroll
@@ -1354,7 +1379,9 @@ static inline int preload_one(F* f) {
 }
 int preload_attention() {
   return preload_one(fa_fwd_kernel<true>) | preload_one(fa_fwd_kernel<false>) |
-         preload_one(fa_fwd_persist_kernel) |
+         preload_one(fa_fwd_persist_kernel<0>) | preload_one(fa_fwd_persist_kernel<1>) |
+         preload_one(fa_fwd_persist_kernel<2>) | preload_one(fa_fwd_persist_kernel<3>) |
+         preload_one(fa_fwd_persist_kernel<4>) | preload_one(fa_fwd_persist_kernel<5>) |
          preload_one(fa_bwd_kernel<true>) | preload_one(fa_bwd_kernel<false>) | preload_one(fa_bwd_pre_kernel) |
          preload_one(attn_combine_scale_kernel) | preload_one(attn_combine_finish_kernel);
 }
@@ -1400,7 +1427,17 @@ extern "C" int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void*
                          FA_FWD_SMEM);
     cudaFuncSetAttribute(fa_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FA_FWD_SMEM_PT);
-    cudaFuncSetAttribute(fa_fwd_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(fa_fwd_persist_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_FWD_SMEM_PERSIST);
+    cudaFuncSetAttribute(fa_fwd_persist_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_FWD_SMEM_PERSIST);
+    cudaFuncSetAttribute(fa_fwd_persist_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_FWD_SMEM_PERSIST);
+    cudaFuncSetAttribute(fa_fwd_persist_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_FWD_SMEM_PERSIST);
+    cudaFuncSetAttribute(fa_fwd_persist_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FA_FWD_SMEM_PERSIST);
+    cudaFuncSetAttribute(fa_fwd_persist_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FA_FWD_SMEM_PERSIST);
     configured = true;
   }
@@ -1410,8 +1447,27 @@ extern "C" int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void*
   if (mode == 0) {
     const int64_t work = (s / FA_BM) * B * H;
     const int64_t slots = 2 * (int64_t)num_sms();
-    fa_fwd_persist_kernel<<<(unsigned)(work < slots ? work : slots), 192, FA_FWD_SMEM_PERSIST,
-                            st>>>(mq, mk, mv, p);
+    // MPEXEC_FA_FWD_EMU=k: k of every eight exponent pairs on the FMA pipe (0-5).
+    // At B=8, H=32, s=1024: 0 -> 106.5 us, 1 -> 101.7, 2 -> 98.8, 3 -> 97.0 (default),
+    // 4 -> 104.2, 5 -> 109.2 (profiles/r2/fa_fwd_exp2_emulation.txt)
+    static const int emu = [] {
+      const char* e = getenv("MPEXEC_FA_FWD_EMU");
+      const int v = e ? atoi(e) : 3;
+      return v < 0 ? 0 : (v > 5 ? 5 : v);
+    }();
+    const unsigned nb = (unsigned)(work < slots ? work : slots);
+    if (emu == 5)
+      fa_fwd_persist_kernel<5><<<nb, 192, FA_FWD_SMEM_PERSIST, st>>>(mq, mk, mv, p);
+    else if (emu == 4)
+      fa_fwd_persist_kernel<4><<<nb, 192, FA_FWD_SMEM_PERSIST, st>>>(mq, mk, mv, p);
+    else if (emu == 3)
+      fa_fwd_persist_kernel<3><<<nb, 192, FA_FWD_SMEM_PERSIST, st>>>(mq, mk, mv, p);
+    else if (emu == 2)
+      fa_fwd_persist_kernel<2><<<nb, 192, FA_FWD_SMEM_PERSIST, st>>>(mq, mk, mv, p);
+    else if (emu == 1)
+      fa_fwd_persist_kernel<1><<<nb, 192, FA_FWD_SMEM_PERSIST, st>>>(mq, mk, mv, p);
+    else
+      fa_fwd_persist_kernel<0><<<nb, 192, FA_FWD_SMEM_PERSIST, st>>>(mq, mk, mv, p);
   } else {
     dim3 grid((unsigned)(s / FA_BM), (unsigned)(B * H));
     if (mode == 2)
