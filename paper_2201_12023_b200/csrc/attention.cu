@@ -151,12 +151,26 @@ __device__ __forceinline__ void sts32(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
 
+// diagnostics: %globaltimer stamp `k` of tile g (query tile in the backward, key tile
+// in the forward).  Compiled in only with
+// -DMP_FA_TRACE (MPEXEC_NVCC_EXTRA) and written when MPEXEC_FA_BWD_TRACE names a file
+__device__ __forceinline__ void fa_stamp(long long* trace, int g, int k) {
+#ifdef MP_FA_TRACE
+  if (trace && g < 1024) {
+    long long ts;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ts));
+    trace[((int64_t)blockIdx.x * 1024 + g) * 8 + k] = ts;
+  }
+#endif
+}
+
 struct FaFwdParams {
   int B, H, s, ld;
   int kv0, nkv;      // key range: tiles [kv0/128, kv0/128 + nkv) of every sequence
   float scale_log2;  // log2(e) / sqrt(d)
   uint16_t* O;
   float* lse;        // [B*H, s]
+  long long* trace;  // diagnostics (MPEXEC_FA_FWD_TRACE, -DMP_FA_TRACE)
 };
 
 // smem: Q 16K | K[2] 32K | V 16K | P 32K | barriers  (97 KB: two CTAs per SM).
@@ -608,6 +622,7 @@ __global__ void __launch_bounds__(192, 2)
         for (int kk = 0; kk < FA_D / 16; ++kk)
           tc_mma_f16(tS, umma_desc_sw128(q_base + kk * 32, 16, 1024),
                      umma_desc_sw128(k_base + kk * 32, 16, 1024), id_s, kk > 0);
+        fa_stamp(p.trace, Jn, 7);
         tc_commit(s_full);
         tc_commit(&k_empty[st]);
         if (jn == n_kv - 1) tc_commit(&q_empty[qs]);
@@ -624,10 +639,12 @@ __global__ void __launch_bounds__(192, 2)
           if (j == 0 && tt > 0) mbar_wait(o_free, (tt - 1) & 1);
           const int st = J & 1;
           mbar_wait(&v_full[st], (J >> 1) & 1);
+          fa_stamp(p.trace, J, 4);
           const uint32_t vb = v_base + st * FA_TILE;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             mbar_wait(h ? p_full1 : p_full, J & 1);
+            fa_stamp(p.trace, J, 5 + h);
             tc_fence_after();
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4) {
@@ -654,6 +671,7 @@ __global__ void __launch_bounds__(192, 2)
       float l = 0.f;
       for (int j = 0; j < n_kv; ++j, ++J) {
         mbar_wait(s_full, J & 1);
+        if (warp == 2 && lane == 0) fa_stamp(p.trace, J, 0);
         tc_fence_after();
         uint32_t sv[4][32];
 #pragma unroll
@@ -740,9 +758,11 @@ __global__ void __launch_bounds__(192, 2)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full1);
+        if (warp == 2 && lane == 0) fa_stamp(p.trace, J, 1);
       }
       // epilogue: O / l -> bf16, then release O for the next tile's first P V
       mbar_wait(o_done, (J - 1) & 1);
+      if (warp == 2 && lane == 0) fa_stamp(p.trace, J - 1, 2);
       tc_fence_after();
       const float inv = 1.f / l;
       uint16_t* orow = p.O + (int64_t)(row0 + qt * FA_BM + r) * p.ld + hh * FA_D;
@@ -765,6 +785,7 @@ __global__ void __launch_bounds__(192, 2)
         dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
       p.lse[(int64_t)bh * p.s + qt * FA_BM + r] = logf(l) + m_used * 0.6931471805599453f;
+      if (warp == 2 && lane == 0) fa_stamp(p.trace, J - 1, 3);
     }
   }
 
@@ -810,17 +831,6 @@ constexpr int FA_BWD_THREADS = 448;   // TMA, MMA, 8 P/dS warps, 4 dQ warps
 // form), so P^T costs neither shared-memory stores nor shared-memory operand reads
 // (the backward is bound by shared-memory bandwidth); the dQ accumulator is
 // single-buffered to make room for it.
-// diagnostics: %globaltimer stamp `k` of query tile g.  Compiled in only with
-// -DMP_FA_TRACE (MPEXEC_NVCC_EXTRA) and written when MPEXEC_FA_BWD_TRACE names a file
-__device__ __forceinline__ void fa_stamp(long long* trace, int g, int k) {
-#ifdef MP_FA_TRACE
-  if (trace && g < 1024) {
-    long long ts;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ts));
-    trace[((int64_t)blockIdx.x * 1024 + g) * 8 + k] = ts;
-  }
-#endif
-}
 
 template <bool PT>
 __global__ void __launch_bounds__(FA_BWD_THREADS, 1)
@@ -1444,6 +1454,16 @@ extern "C" int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void*
   FaFwdParams p{(int)B, (int)H, (int)s, (int)ld, (int)kv0, (int)(kv_len / FA_BN),
                 scale * 1.4426950408889634f, reinterpret_cast<uint16_t*>(o), lse};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // MPEXEC_FA_FWD_TRACE=<file>: diagnostics only (stamps need -DMP_FA_TRACE); every launch
+  // syncs and overwrites <file> with int64 stamps [grid][1024][8]
+  static const char* trace_path = getenv("MPEXEC_FA_FWD_TRACE");
+  static long long* trace_buf = nullptr;
+  const size_t trace_n = (size_t)2 * num_sms() * 1024 * 8;
+  if (trace_path && mode == 0) {
+    if (!trace_buf) cudaMalloc(&trace_buf, trace_n * sizeof(long long));
+    cudaMemsetAsync(trace_buf, 0xff, trace_n * sizeof(long long), st);
+    p.trace = trace_buf;
+  }
   if (mode == 0) {
     const int64_t work = (s / FA_BM) * B * H;
     const int64_t slots = 2 * (int64_t)num_sms();
@@ -1474,6 +1494,16 @@ extern "C" int mp_attn_fwd_kv(const void* q, const void* k, const void* v, void*
       fa_fwd_kernel<false><<<grid, 192, FA_FWD_SMEM, st>>>(mq, mk, mv, p);
     else
       fa_fwd_kernel<true><<<grid, 192, FA_FWD_SMEM_PT, st>>>(mq, mk, mv, p);
+  }
+  if (p.trace) {
+    long long* h = (long long*)malloc(trace_n * sizeof(long long));
+    cudaMemcpyAsync(h, trace_buf, trace_n * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE* fp = fopen(trace_path, "wb")) {
+      fwrite(h, sizeof(long long), trace_n, fp);
+      fclose(fp);
+    }
+    free(h);
   }
   MP_CHECK_LAUNCH();
   return 0;
