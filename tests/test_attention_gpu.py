@@ -26,8 +26,10 @@ def ref_attention(q, k, v, B, H, s, d):
     return o.permute(0, 2, 1, 3).reshape(B * s, H * d), lse.reshape(B * H, s)
 
 
+# (3, 40, 1024, 64): 960 work tiles, so both persistent kernels loop over several tiles
+# per CTA with an uneven last round (forward: 296 CTAs, backward: 148)
 @pytest.mark.parametrize("B,H,s,extra", [(1, 1, 128, 0), (2, 4, 256, 0), (2, 4, 1024, 0),
-                                         (1, 2, 384, 128)])
+                                         (1, 2, 384, 128), (3, 40, 1024, 64)])
 def test_attention_forward_backward(B, H, s, extra):
     torch.manual_seed(0)
     d = 64
@@ -59,3 +61,23 @@ def test_attention_rejects_bad_head_dim():
     lse = torch.zeros(1, 128, device="cuda")
     with pytest.raises(native.NativeError):
         native.attn_fwd(x, x, x, x, lse, 1, 1, 128, 128, 0.1)
+
+
+def test_attention_forward_key_range():
+    """kv_range=(kv0, len): O and LSE over that key slice only (the key-split path)."""
+    torch.manual_seed(1)
+    B, H, s, d = 2, 40, 1024, 64
+    kv0, kvl = 256, 512
+    q, k, v = (torch.randn(B * s, H * d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    o = torch.empty_like(q)
+    lse = torch.empty(B * H, s, device="cuda", dtype=torch.float32)
+    native.attn_fwd(q, k, v, o, lse, B, H, s, d, 1.0 / math.sqrt(d), kv_range=(kv0, kvl))
+
+    def heads(t):
+        return t.float().view(B, s, H, d).permute(0, 2, 1, 3)
+    qh, kh, vh = heads(q), heads(k)[:, :, kv0:kv0 + kvl], heads(v)[:, :, kv0:kv0 + kvl]
+    sc = qh @ kh.transpose(-1, -2) / math.sqrt(d)
+    ro = (torch.softmax(sc, -1) @ vh).permute(0, 2, 1, 3).reshape(B * s, H * d)
+    assert rel(o, ro) < 1e-2
+    assert rel(lse, torch.logsumexp(sc, -1).reshape(B * H, s)) < 1e-3
+
